@@ -1,0 +1,40 @@
+# Build everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> synthgen, oracle, CUDA library
+#   make host       -> synthgen + oracle only (no nvcc)
+# No -march=native: the GPU box's host CPU may differ from the build box.
+
+CC      := $(shell test -x /usr/bin/gcc && echo /usr/bin/gcc || echo gcc)
+NVCC    ?= /usr/local/cuda/bin/nvcc
+PYTHON  ?= python
+
+CUDA_HOME ?= /usr/local/cuda
+NCCL_INC  := $(shell $(PYTHON) -c "import nvidia.nccl,os;print(os.path.join(list(nvidia.nccl.__path__)[0],'include'))" 2>/dev/null)
+
+SG_LIB  := synthgen/libsynthgen.so
+OR_LIB  := oracle/liboracle.so
+MM_LIB  := paper_2408_15384_b200/libmm_b200.so
+
+MM_SRCS := $(wildcard paper_2408_15384_b200/csrc/*.cu) $(wildcard paper_2408_15384_b200/csrc/*.cpp)
+MM_HDRS := $(wildcard paper_2408_15384_b200/csrc/*.cuh) $(wildcard paper_2408_15384_b200/csrc/*.h) include/mm.h
+
+GENCODE := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -std=c++17 -O3 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Iinclude -Ipaper_2408_15384_b200/csrc $(if $(NCCL_INC),-I$(NCCL_INC)) \
+           --expt-relaxed-constexpr -Xptxas -v
+
+.PHONY: all host clean
+all: $(SG_LIB) $(OR_LIB) $(MM_LIB)
+host: $(SG_LIB) $(OR_LIB)
+
+$(SG_LIB): synthgen/synthgen.c
+	$(CC) -O2 -fopenmp -fPIC -shared -o $@ $< -lm
+
+$(OR_LIB): oracle/mmref.c
+	$(CC) -O3 -fopenmp -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
+
+$(MM_LIB): $(MM_SRCS) $(MM_HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(MM_SRCS) -ldl 2> paper_2408_15384_b200/build.log || (cat paper_2408_15384_b200/build.log; exit 1)
+	@grep -E "registers|spill|error" paper_2408_15384_b200/build.log | head -40 || true
+
+clean:
+	rm -f $(SG_LIB) $(OR_LIB) $(MM_LIB)
