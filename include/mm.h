@@ -1,0 +1,144 @@
+/*
+ * mm.h — C-ABI of the B200-native dense product C = A·B.
+ *
+ * The operation (§III, displayed equation):
+ *     C[i][j] = Σ_{k=1..n} A[i][k] · B[k][j],   A is m×n, B is n×p, C is m×p,
+ * i.e. each element is the dot product of row i of A and column j of B
+ * (PAPER.md:62-74), for all i ≤ m, j ≤ p.
+ *
+ * Layout: every matrix is dense ROW-MAJOR ("C ... stores data in row-major
+ * order"): element (i,j) of an r×c matrix lives at i*c + j, so
+ * the leading dimensions are n (A), p (B) and p (C).  No transposes, no α/β.
+ *
+ * Types (mm_dtype, input → output):
+ *   MM_F64      double   × double   → double   (the paper's precision)
+ *   MM_BF16_F32 bfloat16 × bfloat16 → float    (FP32 accumulate; BASELINE.json config 3)
+ *   MM_S8_S32   int8     × int8     → int32    (INT32 accumulate, exact while
+ *                                               n·128² < 2^31; BASELINE.json config 2)
+ *
+ * Ownership: the caller owns A, B, C, the optional workspace and the stream.
+ * The context owns only device properties, a device error word and the
+ * small internal buffers it allocates for padding / host staging.
+ *
+ * Asynchrony: device-pointer calls enqueue on `stream` and return; C is valid
+ * once the stream reaches that point.  A and B must not change before then.
+ * Launch-time errors are returned; in-kernel errors (a pipeline wait that
+ * timed out) are latched in the context's device error word and reported by
+ * mm_sync_check().
+ *
+ * Errors: every call returns an mm_status; on failure mm_last_error(ctx)
+ * names the offending argument (shapes included).  Status codes 0/1/2 mirror
+ * SPEC.md:498 (0 ok, 1 runtime failure, 2 usage error).
+ *
+ * Thread safety: one context per host thread at a time; distinct contexts are
+ * independent.  No global state besides lazily resolved driver/NCCL symbols.
+ */
+#ifndef MM_B200_H
+#define MM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { MM_F64 = 0, MM_BF16_F32 = 1, MM_S8_S32 = 2 } mm_dtype;
+
+typedef enum {
+  MM_OK = 0,
+  MM_ERR_RUNTIME = 1,     /* CUDA / NCCL failure, or a device-side pipeline timeout */
+  MM_ERR_USAGE = 2,       /* bad argument: dims < 1, NULL pointer, bad enum, overlap of C with A/B */
+  MM_ERR_UNSUPPORTED = 3, /* no sm_100a device, or sizes beyond TMA / int64 limits */
+  MM_ERR_WORKSPACE = 4    /* an internal allocation failed */
+} mm_status;
+
+typedef struct mm_ctx mm_ctx;
+
+/* Create a context bound to CUDA `device` (must be sm_100).  `workspace` is an
+ * optional caller-owned device buffer (may be NULL / 0 bytes); it is used for
+ * the padding path before the context allocates its own.  *out receives the
+ * context.  Errors: MM_ERR_USAGE (out NULL), MM_ERR_UNSUPPORTED (not sm_100),
+ * MM_ERR_RUNTIME (CUDA failure). */
+mm_status mm_create(int device, void* workspace, size_t workspace_bytes, mm_ctx** out);
+
+/* Free the context and its internal buffers (never the caller's). NULL is a no-op. */
+void mm_destroy(mm_ctx* ctx);
+
+/* C := A·B on the device.  A (m×n), B (n×p), C (m×p) are device pointers,
+ * row-major, element types per `dtype`.  m, n, p ≥ 1.  Any base alignment and
+ * any m, n, p are accepted: operands whose base or row pitch is not a
+ * multiple of 16 bytes are first copied into a zero-padded buffer (coalesced
+ * 16-byte path), otherwise the kernels read them in place through TMA.
+ * `stream` is a cudaStream_t (NULL = legacy default stream). */
+mm_status mm_gemm(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
+                  const void* A, const void* B, void* C, void* stream);
+
+/* Same product with HOST operands: A, B, C are host pointers (pinned memory
+ * gives full PCIe bandwidth; pageable works).  Copies A and B to the device,
+ * computes, copies C back, in row blocks so that the host↔device copies of
+ * one block overlap the product of the previous one (the paper's row
+ * partition, applied to the PCIe link).  Synchronous: returns
+ * after C is written on the host. */
+mm_status mm_gemm_host(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
+                       const void* A, const void* B, void* C, void* stream);
+
+/* Synchronize `stream` and report any device-side error latched since the
+ * last call (MM_ERR_RUNTIME with a message), then clear it. */
+mm_status mm_sync_check(mm_ctx* ctx, void* stream);
+
+const char* mm_status_string(mm_status s);
+const char* mm_last_error(const mm_ctx* ctx);
+
+/* ------------------------------------------------------------------ sharded
+ * Multi-GPU products, one process per GPU (§III-B2
+ * "Processes"; SUMMA named at PAPER.md:135).  Collective: every rank calls
+ * with identical (m, n, p, dtype, layout, grid, flags, root).
+ *
+ * MM_ROW_BLOCK: C is split by row blocks of A (the paper's row partition of
+ *   the outer loop, across processes).  Rank r owns rows
+ *   [row0, row0+rows) from mm_shard_range(m, G, r, ...) of A and C; B is
+ *   replicated.  A_local is (rows × n), C_local is (rows × p).
+ *   flags: MM_BCAST_B — B is valid only on `root` and is broadcast first
+ *          (B_local must be an n×p buffer on every rank);
+ *          MM_GATHER_C — after the product, the full m×p C is assembled on
+ *          `root` into C_full (ignored elsewhere).
+ * MM_SUMMA_2D: ranks form a grid_rows × grid_cols grid (G = grid_rows*grid_cols),
+ *   rank r ↔ (r / grid_cols, r % grid_cols).  Rank (i,j) owns block (i,j)
+ *   of A (row block i of m, column block j of n), of B (row block i of n,
+ *   column block j of p) and of C (row block i of m, column block j of p),
+ *   blocks by mm_shard_range on each axis.  k-panels of A are broadcast along
+ *   grid rows and of B along grid columns; local products accumulate.
+ *
+ * nccl_comm is an ncclComm_t spanning exactly the G ranks (e.g. torch's
+ * ProcessGroupNCCL._comm_ptr()).  The library resolves NCCL symbols at run
+ * time from the libnccl.so.2 already loaded in the process.
+ */
+typedef enum { MM_ROW_BLOCK = 0, MM_SUMMA_2D = 1 } mm_layout;
+enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u };
+
+mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
+                          mm_layout layout, int grid_rows, int grid_cols,
+                          const void* A_local, void* B_local, void* C_local, void* C_full,
+                          unsigned flags, int root, void* nccl_comm, void* stream);
+
+/* Contiguous block partition of `total` items over G parts:
+ * part r gets [start, start+count); the first parts get ⌈total/G⌉, the
+ * last non-empty part is short, surplus parts (G > total) are empty. */
+void mm_shard_range(int64_t total, int G, int r, int64_t* start, int64_t* count);
+
+/* SUMMA k-panel schedule for an n-long contraction over a grid_rows × grid_cols
+ * grid with target panel width `panel`: panel t covers k in [k0[t], k0[t]+kw[t]),
+ * never straddles a column block of A (owner a_col[t]) nor a row block of B
+ * (owner b_row[t]).  Returns the number of panels, writing at most `cap`.
+ * Pure host logic (tested without a GPU). */
+int mm_summa_panels(int64_t n, int grid_rows, int grid_cols, int64_t panel, int cap,
+                    int64_t* k0, int64_t* kw, int* a_col, int* b_row);
+
+/* Library/version info: "mm_b200 <version> sm_100a". */
+const char* mm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MM_B200_H */

@@ -1,0 +1,178 @@
+"""paper_2408_15384_b200 — B200-native (sm_100a) dense product C = A·B.
+
+The paper's hot path (§III): C[i][j] = Σ_k A[i][k]·B[k][j]
+for an m×n A and an n×p B, row-major.  The compute runs in
+libmm_b200.so (tcgen05 for BF16/INT8, DMMA for FP64, TMA-fed); this module
+marshals torch tensors into the C-ABI of include/mm.h.  PyTorch supplies only
+device memory, streams and process groups.
+
+    import paper_2408_15384_b200 as mm
+    C = mm.gemm(A, B)            # A, B on cuda: float64 | bfloat16 | int8
+    C = mm.gemm_host(A, B)       # A, B on the host (pinned for full PCIe rate)
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import torch
+
+from . import _lib
+from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_ROW_BLOCK, MM_S8_S32, MM_SUMMA_2D)
+
+__all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "MMError", "Context",
+           "sync_check", "version", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
+           "MM_BCAST_B", "MM_GATHER_C"]
+
+IN_DTYPE = {torch.float64: MM_F64, torch.bfloat16: MM_BF16_F32, torch.int8: MM_S8_S32}
+OUT_DTYPE = {MM_F64: torch.float64, MM_BF16_F32: torch.float32, MM_S8_S32: torch.int32}
+
+
+class MMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{_lib.load().mm_status_string(status).decode()}: {msg}")
+
+
+class Context:
+    """Owns one mm_ctx (per device, per thread)."""
+
+    def __init__(self, device: int = 0, workspace: torch.Tensor | None = None):
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        ws_ptr = workspace.data_ptr() if workspace is not None else None
+        ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        st = lib.mm_create(device, ws_ptr, ws_bytes, ctypes.byref(h))
+        if st != 0:
+            raise MMError(st, f"mm_create(device={device}) failed")
+        self.handle = h
+        self.device = device
+        self._ws = workspace
+
+    def check(self, st: int):
+        if st != 0:
+            raise MMError(st, _lib.load().mm_last_error(self.handle).decode())
+
+    def close(self):
+        if self.handle:
+            _lib.load().mm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_local = threading.local()
+
+
+def context(device: int | None = None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device()
+    cache = getattr(_local, "ctx", None)
+    if cache is None:
+        cache = _local.ctx = {}
+    if device not in cache:
+        cache[device] = Context(device)
+    return cache[device]
+
+
+def version() -> str:
+    return _lib.load().mm_version().decode()
+
+
+def _check_operands(A: torch.Tensor, B: torch.Tensor):
+    if A.dim() != 2 or B.dim() != 2:
+        raise ValueError(f"A and B must be 2-D, got {tuple(A.shape)} and {tuple(B.shape)}")
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"inner dimensions differ: A is {tuple(A.shape)}, B is {tuple(B.shape)}")
+    if A.dtype != B.dtype or A.dtype not in IN_DTYPE:
+        raise TypeError(f"A and B must share a dtype in {list(IN_DTYPE)}; got {A.dtype}, {B.dtype}")
+    if not (A.is_contiguous() and B.is_contiguous()):
+        raise ValueError("A and B must be contiguous row-major")
+    return A.shape[0], A.shape[1], B.shape[1], IN_DTYPE[A.dtype]
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
+         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """C = A·B on the GPU (async on `stream`, default: torch's current stream)."""
+    m, n, p, dt = _check_operands(A, B)
+    if not A.is_cuda or A.device != B.device:
+        raise ValueError("gemm expects A and B on the same CUDA device (use gemm_host for host operands)")
+    if out is None:
+        out = torch.empty((m, p), dtype=OUT_DTYPE[dt], device=A.device)
+    elif out.shape != (m, p) or out.dtype != OUT_DTYPE[dt] or not out.is_contiguous() or out.device != A.device:
+        raise ValueError(f"out must be a contiguous {OUT_DTYPE[dt]} ({m}, {p}) tensor on {A.device}")
+    ctx = context(A.device.index)
+    s = stream if stream is not None else torch.cuda.current_stream(A.device)
+    ctx.check(_lib.load().mm_gemm(ctx.handle, m, n, p, dt, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                  s.cuda_stream))
+    return out
+
+
+def gemm_host(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, device: int = 0) -> torch.Tensor:
+    """C = A·B with host operands (copies in, computes, copies out; synchronous)."""
+    m, n, p, dt = _check_operands(A, B)
+    if A.is_cuda or B.is_cuda:
+        raise ValueError("gemm_host expects host tensors")
+    if out is None:
+        out = torch.empty((m, p), dtype=OUT_DTYPE[dt], pin_memory=A.is_pinned())
+    ctx = context(device)
+    with torch.cuda.device(device):
+        s = torch.cuda.current_stream(device)
+        ctx.check(_lib.load().mm_gemm_host(ctx.handle, m, n, p, dt, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                           s.cuda_stream))
+    return out
+
+
+def sync_check(device: int | None = None, stream: torch.cuda.Stream | None = None):
+    """Synchronize and raise if a kernel latched a pipeline error."""
+    ctx = context(device)
+    s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
+    ctx.check(_lib.load().mm_sync_check(ctx.handle, s.cuda_stream))
+
+
+def shard_range(total: int, G: int, r: int) -> tuple[int, int]:
+    """(start, count) of part r of `total` split over G parts (⌈total/G⌉ rule)."""
+    s, c = ctypes.c_int64(), ctypes.c_int64()
+    _lib.load().mm_shard_range(total, G, r, ctypes.byref(s), ctypes.byref(c))
+    return s.value, c.value
+
+
+def summa_panels(n: int, grid_rows: int, grid_cols: int, panel: int):
+    """SUMMA k-panel schedule: list of (k0, kw, a_col_owner, b_row_owner)."""
+    lib = _lib.load()
+    cnt = lib.mm_summa_panels(n, grid_rows, grid_cols, panel, 0, None, None, None, None)
+    k0 = (ctypes.c_int64 * cnt)()
+    kw = (ctypes.c_int64 * cnt)()
+    ao = (ctypes.c_int * cnt)()
+    bo = (ctypes.c_int * cnt)()
+    lib.mm_summa_panels(n, grid_rows, grid_cols, panel, cnt, k0, kw, ao, bo)
+    return [(k0[i], kw[i], ao[i], bo[i]) for i in range(cnt)]
+
+
+def _nccl_comm_ptr(group) -> int:
+    import torch.distributed as dist
+    pg = group if group is not None else dist.group.WORLD
+    backend = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+    return backend._comm_ptr()
+
+
+def gemm_sharded(m: int, n: int, p: int, dtype: torch.dtype, A_local: torch.Tensor | None,
+                 B_local: torch.Tensor, C_local: torch.Tensor | None, *, layout: int = MM_ROW_BLOCK,
+                 grid: tuple[int, int] = (0, 0), flags: int = 0, root: int = 0,
+                 C_full: torch.Tensor | None = None, group=None, stream: torch.cuda.Stream | None = None):
+    """Collective product over an NCCL process group (see include/mm.h, mm_gemm_sharded)."""
+    dt = IN_DTYPE[dtype]
+    dev = B_local.device
+    ctx = context(dev.index)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    comm = _nccl_comm_ptr(group)
+
+    def ptr(t):
+        return t.data_ptr() if t is not None and t.numel() > 0 else None
+    ctx.check(_lib.load().mm_gemm_sharded(ctx.handle, m, n, p, dt, layout, grid[0], grid[1], ptr(A_local),
+                                          ptr(B_local), ptr(C_local), ptr(C_full), flags, root, comm,
+                                          s.cuda_stream))

@@ -1,0 +1,47 @@
+// ctx.h — the mm_ctx object and internal helpers shared by the ABI translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "mm.h"
+
+struct mm_ctx {
+  int device = 0;
+  int num_sms = 0;
+  int cc_major = 0, cc_minor = 0;
+  void* user_ws = nullptr;
+  size_t user_ws_bytes = 0;
+  void* ws = nullptr;  // internal, grow-only (padding path)
+  size_t ws_bytes = 0;
+  int* d_err = nullptr;  // device error word (pipeline timeouts)
+  // mm_gemm_host staging
+  void* hbuf[3] = {nullptr, nullptr, nullptr};
+  size_t hbuf_bytes[3] = {0, 0, 0};
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  // sharded scratch (panels, gathered rows)
+  void* sbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t sbuf_bytes[4] = {0, 0, 0, 0};
+  void* row_comm = nullptr;  // SUMMA sub-communicators (ncclComm_t), cached per parent/grid
+  void* col_comm = nullptr;
+  void* split_parent = nullptr;
+  int split_rows = 0, split_cols = 0;
+  std::string last_error;
+};
+
+namespace mmb {
+
+mm_status set_err(mm_ctx* ctx, mm_status s, const char* fmt, ...);
+size_t dtype_in_size(mm_dtype t);
+size_t dtype_out_size(mm_dtype t);
+// grow-only device buffer owned by ctx (synchronizes the device before freeing an old buffer)
+mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need);
+// internal C (+)= A·B with explicit leading dimensions (elements); beta_one only for MM_F64.
+mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s);
+
+}  // namespace mmb

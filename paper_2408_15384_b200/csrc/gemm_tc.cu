@@ -1,0 +1,295 @@
+// gemm_tc.cu — C = A·B on the 5th-generation tensor cores (tcgen05) for
+//   BF16 × BF16 → FP32  (kind::f16, FP32 accumulators in TMEM)
+//   INT8 × INT8 → INT32 (kind::i8,  INT32 accumulators in TMEM)
+//
+// The operation is PAPER.md:56-60 (§III); A m×n and B n×p are row-major
+// (PAPER.md:87).  What the paper does on a CPU with cache tiling
+// and row-parallel threads is done here as:
+//   * tiles of C (128·CG × 256) walked by a persistent grid of CTA clusters,
+//     grouped along M so concurrently running tiles share B panels in L2;
+//   * K-slabs of A (K-major) and B (row-major = N-major, consumed as an
+//     MN-major UMMA operand, so B's "columns" need no transpose)
+//     staged by TMA into 128-byte-swizzled shared memory, STAGES deep,
+//     full/empty mbarriers between the producer warp and the MMA warp;
+//   * one thread issues tcgen05.mma into a TMEM accumulator; two accumulators
+//     (2 × 256 columns = all 512) let the epilogue of tile j overlap the
+//     mainloop of tile j+1;
+//   * CG = 2: a CTA pair (cluster of 2) runs one M=256 MMA; each CTA stages
+//     its own 128 rows of A and half of B's 256 columns (halving smem traffic
+//     per SM); the leader issues, commits multicast to both.
+//   * edges (ragged m, n, p): TMA zero-fills out-of-bounds boxes (zeros add
+//     exactly 0 to every sum); stores are predicated per element.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> global).
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mmb {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kBN = 256;  // MMA N (columns of C per tile)
+
+template <bool I8, int CG>
+struct TcCfg {
+  static constexpr int ESZ = I8 ? 1 : 2;
+  static constexpr int BK = 128 / ESZ;        // K elements per stage (one 128-B swizzle atom)
+  static constexpr int UK = I8 ? 32 : 16;     // K per tcgen05.mma
+  static constexpr int KSTEPS = BK / UK;      // 4
+  static constexpr int BM = 128;              // rows of A per CTA
+  static constexpr int BN_CTA = kBN / CG;     // columns of B per CTA
+  static constexpr int BOXN = 128 / ESZ;      // columns per TMA box of B (128 B)
+  static constexpr int NBOX = BN_CTA / BOXN;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int BOX_BYTES = BK * 128;
+  static constexpr int B_BYTES = NBOX * BOX_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (CG == 1) ? 4 : 6;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int M_MMA = 128 * CG;
+  // Instruction descriptor: c_format [4,6), a_format [7,10), b_format [10,13),
+  // a_major [15] = K, b_major [16] = MN, N>>3 at [17,23), M>>4 at [24,29).
+  static constexpr uint32_t IDESC = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                                    ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(M_MMA >> 4) << 24);
+};
+
+struct TileSched {
+  int tiles_m, tiles_n, group_m;
+  __device__ __forceinline__ void tile(int t, int& tm, int& tn) const {
+    const int per_group = group_m * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * group_m;
+    const int gm = min(tiles_m - first_m, group_m);
+    const int r = t - g * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+  }
+};
+
+__device__ __forceinline__ void store_row32(uint32_t* __restrict__ C, int64_t ldc, int64_t row, int64_t col0,
+                                            int64_t M, int64_t N, const uint32_t (&v)[32], bool vec_ok) {
+  if (row >= M) return;
+  uint32_t* dst = C + row * ldc + col0;
+  if (vec_ok && col0 + 32 <= N) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i), "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]),
+                   "r"(v[i + 3])
+                   : "memory");
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (col0 + i < N) dst[i] = v[i];
+  }
+}
+
+template <bool I8, int CG>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
+                   TileSched sched, int num_kb) {
+  using Cfg = TcCfg<I8, CG>;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B alignment (SWIZZLE_128B atoms) of the operand ring.
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_u32);
+  const uint32_t sA = base;
+  const uint32_t sB = base + Cfg::STAGES * Cfg::A_BYTES;
+  uint8_t* bar_area = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  const uint32_t bar0 = smem_u32(bar_area);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (Cfg::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 4));
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const int cluster_idx = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int num_clusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
+  const int num_tiles = sched.tiles_m * sched.tiles_n;
+  int* err = args.err;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 4 * CG);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      bool ok = true;
+      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters) {
+        int tm, tn;
+        sched.tile(t, tm, tn);
+        const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
+        const int n0 = tn * kBN + (int)rank * Cfg::BN_CTA;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
+          const uint32_t sa = sA + stage * Cfg::A_BYTES;
+          const uint32_t sb = sB + stage * Cfg::B_BYTES;
+          const int k0 = kb * Cfg::BK;
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, full_bar(stage), k0, m0);
+#pragma unroll
+            for (int b = 0; b < Cfg::NBOX; ++b)
+              tma_load_2d(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0);
+          } else {
+            const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+#pragma unroll
+            for (int b = 0; b < Cfg::NBOX; ++b)
+              tma_load_2d_pair(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0);
+          }
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (rank == 0 && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int j = 0;
+      bool ok = true;
+      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters, ++j) {
+        const int acc = j & 1;
+        const uint32_t use = (uint32_t)(j >> 1);
+        if (!(CG == 2 ? mbar_wait_cluster(tempty_bar(acc), (use & 1u) ^ 1u, err, 2)
+                      : mbar_wait(tempty_bar(acc), (use & 1u) ^ 1u, err, 2))) { ok = false; break; }
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kBN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if (!mbar_wait(full_bar(stage), phase, err, 3)) { ok = false; break; }
+          tc_fence_after();
+          const uint32_t sa = sA + stage * Cfg::A_BYTES;
+          const uint32_t sb = sB + stage * Cfg::B_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
+            // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); K step = 32 B.
+            const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
+            // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
+            const uint64_t bdesc = umma_desc_sw128(sb + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
+            tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit<CG>(empty_bar(stage));  // frees this smem stage (both CTAs) when the MMAs retire
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+        if (!ok) break;
+        tc_commit<CG>(tfull_bar(acc));  // accumulator ready for the epilogue (both CTAs)
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+    uint32_t* C = reinterpret_cast<uint32_t*>(args.C);
+    const bool vec_ok = ((args.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
+    int j = 0;
+    for (int t = cluster_idx; t < num_tiles; t += num_clusters, ++j) {
+      int tm, tn;
+      sched.tile(t, tm, tn);
+      const int acc = j & 1;
+      const uint32_t use = (uint32_t)(j >> 1);
+      if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
+      tc_fence_after();
+      const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + q * 32 + lane;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * kBN);
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + c * 32, v);
+        tmem_ld_wait();
+        store_row32(C, args.ldc, row, (int64_t)tn * kBN + c * 32, args.M, args.N, v, vec_ok);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
+        else mbar_arrive(tempty_bar(acc));
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<CG>(tmem_base, 512);
+}
+
+template <bool I8, int CG>
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int num_sms,
+                        cudaStream_t s) {
+  using Cfg = TcCfg<I8, CG>;
+  auto kern = gemm_tc_kernel<I8, CG>;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  TileSched sched;
+  sched.tiles_m = (int)((a.M + Cfg::M_MMA - 1) / Cfg::M_MMA);
+  sched.tiles_n = (int)((a.N + kBN - 1) / kBN);
+  sched.group_m = 16;
+  const int num_tiles = sched.tiles_m * sched.tiles_n;
+  const int num_kb = (int)((a.K + Cfg::BK - 1) / Cfg::BK);
+  int clusters = num_sms / CG;
+  if (clusters > num_tiles) clusters = num_tiles;
+  if (clusters < 1) clusters = 1;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a, sched, num_kb);
+}
+
+}  // namespace
+
+void tc_box_dims(bool i8, int cg, uint32_t* a_box, uint32_t* b_box) {
+  const uint32_t esz = i8 ? 1 : 2;
+  a_box[0] = 128 / esz;  // K elements (128 B)
+  a_box[1] = 128;        // rows
+  b_box[0] = 128 / esz;  // N elements (128 B)
+  b_box[1] = 128 / esz;  // K rows (BK)
+  (void)cg;
+}
+
+cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                           int num_sms, cudaStream_t s) {
+  if (i8) return cg == 2 ? launch_impl<true, 2>(tmA, tmB, a, num_sms, s) : launch_impl<true, 1>(tmA, tmB, a, num_sms, s);
+  return cg == 2 ? launch_impl<false, 2>(tmA, tmB, a, num_sms, s) : launch_impl<false, 1>(tmA, tmB, a, num_sms, s);
+}
+
+}  // namespace mmb

@@ -1,0 +1,36 @@
+// kernels.h — host-side launch interface of the device kernels (internal).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mmb {
+
+// Problem as the kernels see it: C (M×N, leading dim ldc elements) = A (M×K) · B (K×N).
+// Paper notation: M = m, K = n, N = p.
+struct GemmArgs {
+  int64_t M, N, K;
+  void* C;
+  int64_t ldc;
+  int beta_one;  // FP64 only: C += A·B (used by SUMMA panels); 0 = overwrite
+  int* err;      // device error word (pipeline timeout codes)
+};
+
+// BF16 (A,B bf16 -> C f32) and INT8 (A,B s8 -> C s32) on tcgen05.
+// tmA: dims {K, M} box {128 B of K, 128 rows}; tmB: dims {N, K} box {128 B of N, BK rows}; both SWIZZLE_128B.
+cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                           int num_sms, cudaStream_t s);
+// Box extents the tensor maps must be encoded with.
+void tc_box_dims(bool i8, int cg, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
+
+// FP64 on DMMA (mma.sync m8n8k4) with TMA-fed smem ring.
+cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int num_sms,
+                            cudaStream_t s);
+void f64_box_dims(uint32_t* a_box, uint32_t* b_box);
+
+// Copy a rows×cols matrix (pitch src_ld elements) into dst (pitch dst_ld >= cols), zero-filling
+// columns [cols, dst_ld).  esize ∈ {1, 2, 8}.  Coalesced 16-byte stores on the destination.
+cudaError_t launch_pack_pad(const void* src, int64_t rows, int64_t cols, int64_t src_ld, void* dst, int64_t dst_ld,
+                            int esize, cudaStream_t s);
+
+}  // namespace mmb

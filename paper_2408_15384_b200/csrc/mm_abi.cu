@@ -1,0 +1,382 @@
+// mm_abi.cu — the C-ABI (include/mm.h): argument validation, context, the
+// planner that picks a kernel and encodes TMA tensor maps, the padding edge
+// path, and the host-buffer pipeline.
+//
+// Operation: C = A·B, A m×n, B n×p, row-major.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "ctx.h"
+#include "kernels.h"
+
+#define MM_VERSION "0.1.0"
+
+namespace mmb {
+
+mm_status set_err(mm_ctx* ctx, mm_status s, const char* fmt, ...) {
+  if (ctx) {
+    char buf[768];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->last_error = buf;
+  }
+  return s;
+}
+
+size_t dtype_in_size(mm_dtype t) { return t == MM_F64 ? 8 : (t == MM_BF16_F32 ? 2 : 1); }
+size_t dtype_out_size(mm_dtype t) { return t == MM_F64 ? 8 : 4; }
+
+mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need) {
+  if (*have >= need && *buf) return MM_OK;
+  if (*buf) {
+    cudaDeviceSynchronize();
+    cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+  }
+  size_t sz = need < 256 ? 256 : need;
+  if (cudaMalloc(buf, sz) != cudaSuccess) {
+    cudaGetLastError();
+    *buf = nullptr;
+    return set_err(ctx, MM_ERR_WORKSPACE, "cudaMalloc(%zu bytes) failed", sz);
+  }
+  *have = sz;
+  return MM_OK;
+}
+
+namespace {
+
+// ---- cuTensorMapEncodeTiled, resolved at run time from the driver (no link-time libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+EncodeTiledFn get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+    else
+      cudaGetLastError();
+  });
+  return g_encode;
+}
+
+// Row-major rows×cols matrix with pitch `ld` elements → 2-D tensor map {cols, rows}.
+mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_t esz, const void* ptr, int64_t rows,
+                    int64_t cols, int64_t ld, const uint32_t box[2], const char* what) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_err(ctx, MM_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (int64_t)esz)};
+  cuuint32_t boxd[2] = {box[0], box[1]};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
+                   (long long)rows, (long long)cols, (long long)ld, (int)r);
+  return MM_OK;
+}
+
+inline bool tma_ok(const void* p, int64_t ld, size_t esz) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * (int64_t)esz) % 16 == 0);
+}
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+bool ranges_overlap(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+int force_cg() {
+  const char* e = getenv("MM_FORCE_CG");
+  if (!e) return 0;
+  int v = atoi(e);
+  return (v == 1 || v == 2) ? v : 0;
+}
+
+}  // namespace
+
+mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s) {
+  const size_t esz = dtype_in_size(dtype);
+  // ---- edge path: operands TMA cannot read in place are copied to a zero-padded pitch.
+  const bool padA = !tma_ok(A, lda, esz);
+  const bool padB = !tma_ok(B, ldb, esz);
+  const int64_t align_el = 16 / (int64_t)esz;
+  const int64_t ldA2 = padA ? round_up(n, align_el) : lda;
+  const int64_t ldB2 = padB ? round_up(p, align_el) : ldb;
+  const size_t bytesA = padA ? (size_t)round_up((int64_t)(m * ldA2 * esz), 256) : 0;
+  const size_t bytesB = padB ? (size_t)round_up((int64_t)(n * ldB2 * esz), 256) : 0;
+  const void* Ause = A;
+  const void* Buse = B;
+  if (padA || padB) {
+    const size_t need = bytesA + bytesB;
+    uint8_t* ws;
+    if (ctx->user_ws && ctx->user_ws_bytes >= need && (reinterpret_cast<uintptr_t>(ctx->user_ws) % 256) == 0) {
+      ws = static_cast<uint8_t*>(ctx->user_ws);
+    } else {
+      mm_status st = ensure_buffer(ctx, &ctx->ws, &ctx->ws_bytes, need);
+      if (st != MM_OK) return st;
+      ws = static_cast<uint8_t*>(ctx->ws);
+    }
+    if (padA) {
+      if (launch_pack_pad(A, m, n, lda, ws, ldA2, (int)esz, s) != cudaSuccess)
+        return set_err(ctx, MM_ERR_RUNTIME, "pack(A) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      Ause = ws;
+    }
+    if (padB) {
+      if (launch_pack_pad(B, n, p, ldb, ws + bytesA, ldB2, (int)esz, s) != cudaSuccess)
+        return set_err(ctx, MM_ERR_RUNTIME, "pack(B) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      Buse = ws + bytesA;
+    }
+  }
+
+  GemmArgs a;
+  a.M = m;
+  a.N = p;
+  a.K = n;
+  a.C = C;
+  a.ldc = ldc;
+  a.beta_one = beta_one;
+  a.err = ctx->d_err;
+
+  CUtensorMap tmA, tmB;
+  uint32_t abox[2], bbox[2];
+  cudaError_t e;
+  if (dtype == MM_F64) {
+    f64_box_dims(abox, bbox);
+    mm_status st = encode_2d(ctx, &tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Ause, m, n, padA ? ldA2 : lda, abox, "A");
+    if (st != MM_OK) return st;
+    st = encode_2d(ctx, &tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
+    if (st != MM_OK) return st;
+    e = launch_gemm_f64(tmA, tmB, a, ctx->num_sms, s);
+  } else {
+    if (beta_one) return set_err(ctx, MM_ERR_UNSUPPORTED, "accumulate (beta=1) is only implemented for MM_F64");
+    const bool i8 = dtype == MM_S8_S32;
+    int cg = force_cg();
+    if (!cg) cg = (m <= 128) ? 1 : 2;
+    tc_box_dims(i8, cg, abox, bbox);
+    const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    mm_status st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
+    if (st != MM_OK) return st;
+    st = encode_2d(ctx, &tmB, dt, esz, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
+    if (st != MM_OK) return st;
+    e = launch_gemm_tc(i8, cg, tmA, tmB, a, ctx->num_sms, s);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, MM_ERR_RUNTIME, "kernel launch failed (m=%lld n=%lld p=%lld dtype=%d): %s", (long long)m,
+                   (long long)n, (long long)p, (int)dtype, cudaGetErrorString(e));
+  }
+  return MM_OK;
+}
+
+}  // namespace mmb
+
+using namespace mmb;
+
+static mm_status validate(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, const void* B,
+                          const void* C) {
+  if (!ctx) return MM_ERR_USAGE;
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32)
+    return set_err(ctx, MM_ERR_USAGE, "unknown dtype %d", (int)dtype);
+  if (m < 1 || n < 1 || p < 1)
+    return set_err(ctx, MM_ERR_USAGE, "dimensions must be >= 1: A is %lld x %lld, B is %lld x %lld", (long long)m,
+                   (long long)n, (long long)n, (long long)p);
+  if (!A || !B || !C) return set_err(ctx, MM_ERR_USAGE, "NULL operand pointer (A=%p B=%p C=%p)", A, B, C);
+  // TMA coordinates are int32 and dims < 2^32; tile indices are int.
+  const int64_t lim = (int64_t)1 << 31;
+  if (m >= lim || n >= lim || p >= lim)
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "dimension >= 2^31 (m=%lld n=%lld p=%lld)", (long long)m, (long long)n,
+                   (long long)p);
+  const size_t ei = dtype_in_size(dtype), eo = dtype_out_size(dtype);
+  const __int128 bA = (__int128)m * n * ei, bB = (__int128)n * p * ei, bC = (__int128)m * p * eo;
+  const __int128 maxb = ((__int128)1 << 62);
+  if (bA > maxb || bB > maxb || bC > maxb) return set_err(ctx, MM_ERR_UNSUPPORTED, "operand byte size overflows int64");
+  if (ranges_overlap(C, (size_t)bC, A, (size_t)bA) || ranges_overlap(C, (size_t)bC, B, (size_t)bB))
+    return set_err(ctx, MM_ERR_USAGE, "C (%lld x %lld) overlaps A or B", (long long)m, (long long)p);
+  return MM_OK;
+}
+
+extern "C" {
+
+__attribute__((visibility("default"))) const char* mm_version(void) { return "mm_b200 " MM_VERSION " sm_100a"; }
+
+__attribute__((visibility("default"))) const char* mm_status_string(mm_status s) {
+  switch (s) {
+    case MM_OK: return "MM_OK";
+    case MM_ERR_RUNTIME: return "MM_ERR_RUNTIME";
+    case MM_ERR_USAGE: return "MM_ERR_USAGE";
+    case MM_ERR_UNSUPPORTED: return "MM_ERR_UNSUPPORTED";
+    case MM_ERR_WORKSPACE: return "MM_ERR_WORKSPACE";
+  }
+  return "MM_ERR_UNKNOWN";
+}
+
+__attribute__((visibility("default"))) const char* mm_last_error(const mm_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : "NULL context";
+}
+
+__attribute__((visibility("default"))) mm_status mm_create(int device, void* workspace, size_t workspace_bytes,
+                                                           mm_ctx** out) {
+  if (!out) return MM_ERR_USAGE;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return MM_ERR_UNSUPPORTED;
+  }
+  if (device < 0 || device >= ndev) return MM_ERR_USAGE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return MM_ERR_RUNTIME;
+  if (prop.major != 10 || prop.minor != 0) return MM_ERR_UNSUPPORTED;  // sm_100a code only
+  mm_ctx* ctx = new mm_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->cc_major = prop.major;
+  ctx->cc_minor = prop.minor;
+  ctx->user_ws = workspace;
+  ctx->user_ws_bytes = workspace ? workspace_bytes : 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, sizeof(int)) != cudaSuccess) {
+    cudaSetDevice(prev);
+    delete ctx;
+    return MM_ERR_RUNTIME;
+  }
+  cudaSetDevice(prev);
+  *out = ctx;
+  return MM_OK;
+}
+
+void mm_release_comms(mm_ctx* ctx);  // shard.cu
+
+__attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
+  if (!ctx) return;
+  cudaDeviceSynchronize();
+  mm_release_comms(ctx);
+  if (ctx->ws) cudaFree(ctx->ws);
+  for (auto& b : ctx->hbuf)
+    if (b) cudaFree(b);
+  for (auto& b : ctx->sbuf)
+    if (b) cudaFree(b);
+  if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+  if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  delete ctx;
+}
+
+__attribute__((visibility("default"))) mm_status mm_gemm(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
+                                                         mm_dtype dtype, const void* A, const void* B, void* C,
+                                                         void* stream) {
+  mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
+  if (st != MM_OK) return st;
+  return gemm_ld(ctx, m, n, p, dtype, A, n, B, p, C, p, 0, static_cast<cudaStream_t>(stream));
+}
+
+__attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void* stream) {
+  if (!ctx) return MM_ERR_USAGE;
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "stream sync failed: %s", cudaGetErrorString(e));
+  int h = 0;
+  if (cudaMemcpy(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "reading the device error word failed");
+  if (h != 0) {
+    cudaMemset(ctx->d_err, 0, sizeof(int));
+    return set_err(ctx, MM_ERR_RUNTIME, "device pipeline wait timed out (code %d)", h);
+  }
+  return MM_OK;
+}
+
+// Host operands: B once, then row blocks of A in / C out on their own streams,
+// so the PCIe copies of block b±1 overlap the product of block b.
+__attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
+                                                              mm_dtype dtype, const void* A, const void* B, void* C,
+                                                              void* stream) {
+  mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
+  if (st != MM_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t ei = dtype_in_size(dtype), eo = dtype_out_size(dtype);
+  if (!ctx->s_in) {
+    if (cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking) != cudaSuccess)
+      return set_err(ctx, MM_ERR_RUNTIME, "stream creation failed");
+  }
+  if ((st = ensure_buffer(ctx, &ctx->hbuf[0], &ctx->hbuf_bytes[0], (size_t)(m * n) * ei)) != MM_OK) return st;
+  if ((st = ensure_buffer(ctx, &ctx->hbuf[1], &ctx->hbuf_bytes[1], (size_t)(n * p) * ei)) != MM_OK) return st;
+  if ((st = ensure_buffer(ctx, &ctx->hbuf[2], &ctx->hbuf_bytes[2], (size_t)(m * p) * eo)) != MM_OK) return st;
+  uint8_t* dA = static_cast<uint8_t*>(ctx->hbuf[0]);
+  uint8_t* dB = static_cast<uint8_t*>(ctx->hbuf[1]);
+  uint8_t* dC = static_cast<uint8_t*>(ctx->hbuf[2]);
+  const uint8_t* hA = static_cast<const uint8_t*>(A);
+  uint8_t* hC = static_cast<uint8_t*>(C);
+
+  // row blocks: ~8 blocks, multiples of 256 rows (one CTA-pair tile height)
+  int64_t rb = round_up((m + 7) / 8, 256);
+  if (rb > m) rb = m;
+  const int64_t nblk = (m + rb - 1) / rb;
+  cudaEvent_t evB, evIn[64], evC[64];
+  if (nblk > 64) rb = round_up((m + 63) / 64, 256);
+  const int64_t nb = (m + rb - 1) / rb;
+  (void)nblk;
+  cudaEventCreateWithFlags(&evB, cudaEventDisableTiming);
+  for (int64_t b = 0; b < nb; ++b) {
+    cudaEventCreateWithFlags(&evIn[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evC[b], cudaEventDisableTiming);
+  }
+  cudaError_t e = cudaSuccess;
+  // the in-stream must not run ahead of earlier work on the caller's stream that reads the buffers
+  cudaEvent_t evStart;
+  cudaEventCreateWithFlags(&evStart, cudaEventDisableTiming);
+  cudaEventRecord(evStart, s);
+  cudaStreamWaitEvent(ctx->s_in, evStart, 0);
+  cudaStreamWaitEvent(ctx->s_out, evStart, 0);
+  e = cudaMemcpyAsync(dB, B, (size_t)(n * p) * ei, cudaMemcpyHostToDevice, ctx->s_in);
+  cudaEventRecord(evB, ctx->s_in);
+  for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
+    const int64_t r0 = b * rb, rows = std::min(rb, m - r0);
+    e = cudaMemcpyAsync(dA + r0 * n * ei, hA + r0 * n * ei, (size_t)(rows * n) * ei, cudaMemcpyHostToDevice,
+                        ctx->s_in);
+    cudaEventRecord(evIn[b], ctx->s_in);
+  }
+  cudaStreamWaitEvent(s, evB, 0);
+  for (int64_t b = 0; b < nb && e == cudaSuccess && st == MM_OK; ++b) {
+    const int64_t r0 = b * rb, rows = std::min(rb, m - r0);
+    cudaStreamWaitEvent(s, evIn[b], 0);
+    st = gemm_ld(ctx, rows, n, p, dtype, dA + r0 * n * ei, n, dB, p, dC + r0 * p * eo, p, 0, s);
+    cudaEventRecord(evC[b], s);
+    cudaStreamWaitEvent(ctx->s_out, evC[b], 0);
+    e = cudaMemcpyAsync(hC + r0 * p * eo, dC + r0 * p * eo, (size_t)(rows * p) * eo, cudaMemcpyDeviceToHost,
+                        ctx->s_out);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(ctx->s_out);
+  cudaStreamSynchronize(s);
+  cudaEventDestroy(evB);
+  cudaEventDestroy(evStart);
+  for (int64_t b = 0; b < nb; ++b) {
+    cudaEventDestroy(evIn[b]);
+    cudaEventDestroy(evC[b]);
+  }
+  if (st != MM_OK) return st;
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "host pipeline failed: %s",
+                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+  return mm_sync_check(ctx, s);
+}
+
+}  // extern "C"
