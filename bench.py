@@ -1,0 +1,392 @@
+"""bench.py — throughput of the B200-native dense product C = A·B.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N   (row-block sharding, one process per GPU)
+
+Workload (config.workload): BASELINE.json configs[3] — BF16 16384×16384·16384×16384
+with FP32 accumulate/output, entries Box–Muller N(0,1) rounded to bf16 from seed 3
+(synthgen/), the config BASELINE.json quotes at 1/2/4/8 B200.  A "step" is one
+pass of the whole hot path: argument validation + plan (TMA maps) + the tcgen05
+kernel (staging, MMA, epilogue, edges).  At N>1 the rows of A and C are split
+into row blocks (mm_shard_range); B is resident on every rank ("resident"
+regime); a second measurement adds the NCCL broadcast of B and gather of C.
+
+`value` = 2·m·n·p of the whole job ÷ max-over-ranks device time per step
+(CUDA events on the launching stream, barrier + synchronize on both sides).
+Operands (1 GiB of A+B, 1 GiB of C) exceed the 126 MB L2, so no flush is needed
+between steps.  `e2e` = the same metric through mm_gemm_host with pinned host
+buffers (H2D of A, B and D2H of C inside the timed region).
+
+The other BASELINE.json configs are timed briefly into `per_config` (device
+inputs drawn with torch's seeded RNG in the same distributions; timing does not
+depend on values) next to cuBLAS on the same shapes.  Parity for every config
+lives in tests/ (pytest -m gpu), not here.
+
+--impl reference: the CPU oracle (oracle/, the paper's triple loop with the
+paper's own row-parallel OpenMP) timed on this host on a bounded
+row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GEMM TFLOPS (2mnp/s) per dtype at 1/2/4/8 B200; fraction of dense peak"
+UNIT = "TFLOP/s"
+M = N_ = P = 16384
+SEED = 3
+WORKLOAD = ("BASELINE.json configs[3]: BF16 16384x16384 . 16384x16384, FP32 accumulate and output, "
+            "entries Box-Muller N(0,1) rounded to bf16 from seed 3, row-major")
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def cpu_count_used():
+    import oracle
+    return oracle.max_threads()
+
+
+def oracle_rows_sample(A_bits, B_bits, nrows, seed=7):
+    """Time the oracle (as it stands) on `nrows` full rows of C; returns (seconds, flops)."""
+    import oracle
+    import synthgen as sg
+    rows = np.unique(sg.sample_indices(seed, sg.ROLE_ROWS, nrows, A_bits.shape[0]))
+    t0 = time.perf_counter()
+    oracle.gemm_bf16_rows(A_bits, B_bits, rows)
+    dt = time.perf_counter() - t0
+    return dt, 2.0 * rows.size * A_bits.shape[1] * B_bits.shape[1], rows.size
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def device_time_steps(fn, steps, warmup, dist=None):
+    """Max-over-ranks device time (ms) per step of `fn` on the current stream."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    return ms / steps
+
+
+def per_launch_ms(fn, reps, flush_buf=None):
+    """Median per-launch device time with optional L2 flush before each launch."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush_buf is not None:
+            flush_buf.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def per_config_table(mm, peaks):
+    """Brief timings of the other BASELINE.json configs at N=1 (ours vs cuBLAS)."""
+    import torch
+    g = torch.Generator(device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    out = {}
+    bf16_peak = peaks["bf16_tflops"]
+    cases = [
+        ("configs[0] FP64 256^3 seed 0", "f64", 256, 256, 256, 30),
+        ("configs[1] FP64 2000x1500x1750 seed 1", "f64", 2000, 1500, 1750, 15),
+        ("configs[2] INT8 4096^3 seed 2", "i8", 4096, 4096, 4096, 15),
+        ("configs[4] FP64 32768^3 seed 4 (1 GPU)", "f64", 32768, 32768, 32768, 2),
+    ]
+    for name, dt, m, n, p, reps in cases:
+        g.manual_seed(hash(name) & 0xFFFF)
+        try:
+            if dt == "f64":
+                A = torch.rand(m, n, device="cuda", dtype=torch.float64, generator=g).mul_(2).sub_(1)
+                B = torch.rand(n, p, device="cuda", dtype=torch.float64, generator=g).mul_(2).sub_(1)
+                ref = lambda: torch.matmul(A, B)  # noqa: E731
+                nominal = 37.0  # HGX-B200 FP64 / FP64-tensor dense, no measured FP64 peak in MEASURED_PEAKS.json
+                peak_note = "nominal FP64 37 TFLOP/s (HGX B200 spec)"
+            else:
+                A = torch.randint(-127, 128, (m, n), device="cuda", dtype=torch.int8, generator=g)
+                B = torch.randint(-127, 128, (n, p), device="cuda", dtype=torch.int8, generator=g)
+                ref = lambda: torch._int_mm(A, B)  # noqa: E731
+                nominal = 2.0 * bf16_peak  # measured bf16 x nominal int8/bf16 ratio (4.5/2.25)
+                peak_note = "measured bf16 burst x 2 (nominal INT8:BF16 ratio)"
+            C = torch.empty(m, p, device="cuda", dtype=torch.float64 if dt == "f64" else torch.int32)
+            flops = 2.0 * m * n * p
+            big = m * n > (1 << 26)
+            t_ours = per_launch_ms(lambda: mm.gemm(A, B, out=C), reps, None if big else flush)
+            mm.sync_check()
+            t_ref = per_launch_ms(ref, reps, None if big else flush)
+            tf = flops / t_ours / 1e9
+            out[name] = {
+                "ms": round(t_ours, 4), "tflops": round(tf, 2), "frac_of_peak": round(tf / nominal, 4),
+                "peak": round(nominal, 1), "peak_note": peak_note,
+                "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
+                "l2": "flushed before each launch" if not big else "operands larger than L2",
+            }
+            del A, B, C
+            torch.cuda.empty_cache()
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"error": str(e)[:200]}
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on this host (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import synthgen as sg
+    A = sg.normal_bf16(SEED, sg.ROLE_A, M, N_)
+    B = sg.normal_bf16(SEED, sg.ROLE_B, N_, P)
+    cores = cpu_count_used()
+    nrows = max(8, cores)
+    for i in range(args.warmup):
+        oracle_rows_sample(A, B, max(1, cores // 2), seed=100 + i)
+    secs, flops, rows = 0.0, 0.0, 0
+    for i in range(args.steps):
+        dt, fl, nr = oracle_rows_sample(A, B, nrows, seed=200 + i)
+        secs += dt
+        flops += fl
+        rows += nr
+    value = flops / secs / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16->f64 (oracle)",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "m": M, "n": N_, "p": P, "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{rows} full rows of C ({nrows} per step, seeded) of the 16384^3 product"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2408_15384_b200 as mm
+    import synthgen as sg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_
+        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_
+    peaks, peak_src = load_peaks()
+
+    # ---- inputs (synthgen recipe); each rank holds its row block of A and all of B
+    r0, rows = mm.shard_range(M, world, rank)
+    A_full = sg.normal_bf16(SEED, sg.ROLE_A, M, N_)
+    B_host = sg.normal_bf16(SEED, sg.ROLE_B, N_, P)
+    A_host = np.ascontiguousarray(A_full[r0:r0 + rows])
+    A = torch.from_numpy(A_host.view(np.int16)).view(torch.bfloat16).cuda()
+    B = torch.from_numpy(B_host.view(np.int16)).view(torch.bfloat16).cuda()
+    C = torch.empty(rows, P, dtype=torch.float32, device="cuda")
+    flops_total = 2.0 * M * N_ * P
+
+    launches0 = mm.launches()
+    clk = ClockSampler(local)
+    step = (lambda: mm.gemm(A, B, out=C)) if rows > 0 else (lambda: None)
+    # warm-up, then the timed region with clocks sampled during it
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.2)
+    ms = device_time_steps(step, args.steps, 0, dist)
+    clocks = clk.stop()
+    mm.sync_check()
+    launches = mm.launches() - launches0 - args.warmup * (1 if rows > 0 else 0)
+    value = flops_total / (ms * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (the tcgen05 BF16 kernel is the whole step)
+    per_rank_flops = 2.0 * rows * N_ * P
+    achieved = per_rank_flops / (ms * 1e-3) / 1e12 if rows else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("gemm_tc_kernel_bf16_c4_bytes_per_launch")
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
+                "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                "kernel": "gemm_tc_kernel<bf16, CTA pair>", "algorithmic_flops_per_launch": per_rank_flops}
+
+    # ---- with communication (N>1): broadcast B from rank 0, gather C to rank 0, around the product
+    with_comm = None
+    if world > 1:
+        C_full = torch.empty(M, P, dtype=torch.float32, device="cuda") if rank == 0 else None
+
+        def step_comm():
+            mm.gemm_sharded(M, N_, P, torch.bfloat16, A, B, C, layout=mm.MM_ROW_BLOCK,
+                            flags=mm.MM_BCAST_B | mm.MM_GATHER_C, root=0, C_full=C_full)
+        ms_c = device_time_steps(step_comm, max(3, args.steps // 10), 2, dist)
+        with_comm = {"value": flops_total / (ms_c * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_c,
+                     "what": "NCCL broadcast of B from rank 0 + row-block product + gather of C to rank 0"}
+
+    # ---- e2e through the public host-buffer API (pinned buffers, H2D + D2H inside the timed region)
+    Ah = torch.from_numpy(A_host.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Bh = torch.from_numpy(B_host.view(np.int16)).view(torch.bfloat16).pin_memory()
+    Ch = torch.empty(rows, P, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(10, args.steps // 10))
+    for _ in range(2):
+        if rows:
+            mm.gemm_host(Ah, Bh, out=Ch, device=local)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if rows:
+            mm.gemm_host(Ah, Bh, out=Ch, device=local)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": flops_total / e2e_s / 1e12, "unit": UNIT,
+           "h2d_bytes_per_step": int((rows * N_ + N_ * P) * 2 * world),
+           "d2h_bytes_per_step": int(rows * P * 4 * world),
+           "ms_per_step": e2e_s * 1e3, "api": "mm_gemm_host (pinned host A, B, C; synchronous call)"}
+
+    per_config = None
+    if rank == 0 and not args.no_per_config:
+        per_config = per_config_table(mm, peaks)
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = cpu_count_used()
+        nrows = max(8, 2 * cores)
+        secs, fl, nr = oracle_rows_sample(A_full, B_host, nrows)
+        cpu_baseline = {"value": fl / secs / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+                        "sample": f"{nr} seeded full rows of C of the 16384^3 BF16 product "
+                                  f"({fl/1e9:.1f} GFLOP, {secs:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "m": M, "n": N_, "p": P, "seed": SEED,
+                       "parallelism": f"row-block x{world} (B resident on every rank)" if world > 1 else "single GPU",
+                       "l2": "operands larger than L2 (A+B 1 GiB, C 1 GiB vs 126 MB): no flush needed"},
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "with_comm": with_comm, "per_config": per_config,
+            "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
+                                       "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
+                                       "vs_spec_2250": round(value / world / 2250.0, 4)},
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -135,6 +135,10 @@ void mm_shard_range(int64_t total, int G, int r, int64_t* start, int64_t* count)
 int mm_summa_panels(int64_t n, int grid_rows, int grid_cols, int64_t panel, int cap,
                     int64_t* k0, int64_t* kw, int* a_col, int* b_row);
 
+/* Number of kernels this context has launched so far (product, padding and
+ * fix-up kernels; NCCL's own kernels are not counted). */
+uint64_t mm_launches(const mm_ctx* ctx);
+
 /* Library/version info: "mm_b200 <version> sm_100a". */
 const char* mm_version(void);
 

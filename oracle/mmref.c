@@ -122,18 +122,25 @@ void mmref_f64_rows(int64_t m, int64_t n, int64_t p, const double* A, const doub
 /* cols[c] selects output column j = cols[c]; C, D are m × ncols */
 void mmref_f64_cols(int64_t m, int64_t n, int64_t p, const double* A, const double* B,
                     int64_t ncols, const int64_t* cols, double* C, double* D) {
+  /* gather the selected columns of B once (a copy, no arithmetic); the
+   * per-element sum is still s = s + A[i][k]*B[k][j], k ascending */
+  double* Bc = (double*)malloc((size_t)(n * ncols) * sizeof(double));
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t c = 0; c < ncols; ++c) Bc[k * ncols + c] = B[k * p + cols[c]];
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t i = 0; i < m; ++i)
-    for (int64_t c = 0; c < ncols; ++c) {
-      const int64_t j = cols[c];
-      double s = 0.0, d = 0.0;
-      for (int64_t k = 0; k < n; ++k) {
-        s = s + A[i * n + k] * B[k * p + j];
-        d = d + fabs(A[i * n + k] * B[k * p + j]);
+  for (int64_t i = 0; i < m; ++i) {
+    double* c_ = C + i * ncols;
+    double* d_ = D + i * ncols;
+    for (int64_t c = 0; c < ncols; ++c) c_[c] = 0.0, d_[c] = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double a = A[i * n + k];
+      for (int64_t c = 0; c < ncols; ++c) {
+        c_[c] = c_[c] + a * Bc[k * ncols + c];
+        d_[c] = d_[c] + fabs(a * Bc[k * ncols + c]);
       }
-      C[i * ncols + c] = s;
-      D[i * ncols + c] = d;
     }
+  }
+  free(Bc);
 }
 
 /* ------------------------------ BF16 ------------------------------ */

@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_ROW_BLOCK, MM_S8_S32, MM_SUMMA_2D)
 
 __all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "MMError", "Context",
-           "sync_check", "version", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
+           "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
            "MM_BCAST_B", "MM_GATHER_C"]
 
 IN_DTYPE = {torch.float64: MM_F64, torch.bfloat16: MM_BF16_F32, torch.int8: MM_S8_S32}
@@ -77,6 +77,11 @@ def context(device: int | None = None) -> Context:
     if device not in cache:
         cache[device] = Context(device)
     return cache[device]
+
+
+def launches(device: int | None = None) -> int:
+    """Kernels launched so far by this thread's context on `device`."""
+    return int(_lib.load().mm_launches(context(device).handle))
 
 
 def version() -> str:

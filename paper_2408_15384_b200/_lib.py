@@ -17,7 +17,7 @@ MM_BCAST_B, MM_GATHER_C = 1, 2
 # every symbol include/mm.h declares
 EXPORTS = (
     "mm_create", "mm_destroy", "mm_gemm", "mm_gemm_host", "mm_sync_check", "mm_status_string",
-    "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_version",
+    "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_launches", "mm_version",
 )
 
 _i64, _vp, _int, _uint, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_uint, ctypes.c_size_t
@@ -54,6 +54,8 @@ def load():
     lib.mm_shard_range.restype = None
     lib.mm_summa_panels.argtypes = [_i64, _int, _int, _i64, _int, _vp, _vp, _vp, _vp]
     lib.mm_summa_panels.restype = _int
+    lib.mm_launches.argtypes = [_vp]
+    lib.mm_launches.restype = ctypes.c_uint64
     lib.mm_version.argtypes = []
     lib.mm_version.restype = ctypes.c_char_p
     _lib = lib

@@ -30,6 +30,7 @@ struct mm_ctx {
   void* col_comm = nullptr;
   void* split_parent = nullptr;
   int split_rows = 0, split_cols = 0;
+  uint64_t launches = 0;  // kernels launched by this context
   std::string last_error;
 };
 

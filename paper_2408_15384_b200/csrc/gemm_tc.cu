@@ -22,6 +22,8 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> global).
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -254,6 +256,8 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   sched.tiles_m = (int)((a.M + Cfg::M_MMA - 1) / Cfg::M_MMA);
   sched.tiles_n = (int)((a.N + kBN - 1) / kBN);
   sched.group_m = 16;
+  if (const char* e = getenv("MM_GROUP_M")) sched.group_m = atoi(e) > 0 ? atoi(e) : 16;  // tuning knob
+  if (sched.group_m > sched.tiles_m) sched.group_m = sched.tiles_m;
   const int num_tiles = sched.tiles_m * sched.tiles_n;
   const int num_kb = (int)((a.K + Cfg::BK - 1) / Cfg::BK);
   int clusters = num_sms / CG;

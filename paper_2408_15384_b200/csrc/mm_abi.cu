@@ -136,11 +136,13 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (padA) {
       if (launch_pack_pad(A, m, n, lda, ws, ldA2, (int)esz, s) != cudaSuccess)
         return set_err(ctx, MM_ERR_RUNTIME, "pack(A) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      ++ctx->launches;
       Ause = ws;
     }
     if (padB) {
       if (launch_pack_pad(B, n, p, ldb, ws + bytesA, ldB2, (int)esz, s) != cudaSuccess)
         return set_err(ctx, MM_ERR_RUNTIME, "pack(B) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      ++ctx->launches;
       Buse = ws + bytesA;
     }
   }
@@ -177,6 +179,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (st != MM_OK) return st;
     e = launch_gemm_tc(i8, cg, tmA, tmB, a, ctx->num_sms, s);
   }
+  if (e == cudaSuccess) ++ctx->launches;
   if (e != cudaSuccess) {
     cudaGetLastError();
     return set_err(ctx, MM_ERR_RUNTIME, "kernel launch failed (m=%lld n=%lld p=%lld dtype=%d): %s", (long long)m,
@@ -215,6 +218,8 @@ static mm_status validate(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
 extern "C" {
 
 __attribute__((visibility("default"))) const char* mm_version(void) { return "mm_b200 " MM_VERSION " sm_100a"; }
+
+__attribute__((visibility("default"))) uint64_t mm_launches(const mm_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 __attribute__((visibility("default"))) const char* mm_status_string(mm_status s) {
   switch (s) {

@@ -53,6 +53,9 @@ def _load():
     lib.sg_word.restype = _u64
     lib.sg_bf16_from_double.argtypes = [ctypes.c_double]
     lib.sg_bf16_from_double.restype = ctypes.c_uint16
+    for name in ("sg_checksum_f64_off", "sg_checksum_f32_off", "sg_checksum_f64_as_f32_off", "sg_checksum_i32_off"):
+        getattr(lib, name).argtypes = [_vp, _i64, _i64]
+        getattr(lib, name).restype = _u64
     lib.sg_box_muller.argtypes = [ctypes.c_double, ctypes.c_double, _vp, _vp]
     _lib = lib
     return lib
@@ -150,6 +153,16 @@ def checksum(x: np.ndarray, kind: str | None = None) -> int:
     fn = {"f64": lib.sg_checksum_f64, "f32": lib.sg_checksum_f32, "i32": lib.sg_checksum_i32,
           "bf16": lib.sg_checksum_bf16, "i8": lib.sg_checksum_i8}[kind]
     return int(fn(_ptr(x), x.size))
+
+
+def checksum_block(x: np.ndarray, offset: int, kind: str) -> int:
+    """Checksum terms of a block whose first element has global row-major index `offset`
+    (kind: "f64", "f32", or "f64_as_f32" for exactly-representable doubles stored as fp32)."""
+    x = np.ascontiguousarray(x)
+    lib = _load()
+    fn = {"f64": lib.sg_checksum_f64_off, "f32": lib.sg_checksum_f32_off,
+          "f64_as_f32": lib.sg_checksum_f64_as_f32_off, "i32": lib.sg_checksum_i32_off}[kind]
+    return int(fn(_ptr(x), x.size, offset))
 
 
 def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:

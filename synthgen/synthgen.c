@@ -158,36 +158,53 @@ void sg_sample_indices(uint64_t seed, uint64_t role, int64_t count, int64_t limi
 
 static inline uint64_t cs_term(uint64_t bits, int64_t idx) { return fmix64(bits + (uint64_t)(idx + 1) * GOLDEN); }
 
-uint64_t sg_checksum_f64(const double* x, int64_t N) {
+/* `off` = global row-major index of x[0] (checksums of row blocks add up mod 2^64). */
+uint64_t sg_checksum_f64_off(const double* x, int64_t N, int64_t off) {
   uint64_t s = 0;
 #pragma omp parallel for reduction(+ : s) schedule(static)
   for (int64_t i = 0; i < N; ++i) {
     double v = x[i] + 0.0; /* -0.0 -> +0.0 */
     uint64_t b;
     memcpy(&b, &v, 8);
-    s += cs_term(b, i);
+    s += cs_term(b, off + i);
   }
   return s;
 }
+uint64_t sg_checksum_f64(const double* x, int64_t N) { return sg_checksum_f64_off(x, N, 0); }
 
-uint64_t sg_checksum_f32(const float* x, int64_t N) {
+uint64_t sg_checksum_f32_off(const float* x, int64_t N, int64_t off) {
   uint64_t s = 0;
 #pragma omp parallel for reduction(+ : s) schedule(static)
   for (int64_t i = 0; i < N; ++i) {
     float v = x[i] + 0.0f;
     uint32_t b;
     memcpy(&b, &v, 4);
-    s += cs_term((uint64_t)b, i);
+    s += cs_term((uint64_t)b, off + i);
+  }
+  return s;
+}
+uint64_t sg_checksum_f32(const float* x, int64_t N) { return sg_checksum_f32_off(x, N, 0); }
+
+/* checksum of doubles as if they had been stored as fp32 / int32 (exact-int results) */
+uint64_t sg_checksum_f64_as_f32_off(const double* x, int64_t N, int64_t off) {
+  uint64_t s = 0;
+#pragma omp parallel for reduction(+ : s) schedule(static)
+  for (int64_t i = 0; i < N; ++i) {
+    float v = (float)x[i] + 0.0f;
+    uint32_t b;
+    memcpy(&b, &v, 4);
+    s += cs_term((uint64_t)b, off + i);
   }
   return s;
 }
 
-uint64_t sg_checksum_i32(const int32_t* x, int64_t N) {
+uint64_t sg_checksum_i32_off(const int32_t* x, int64_t N, int64_t off) {
   uint64_t s = 0;
 #pragma omp parallel for reduction(+ : s) schedule(static)
-  for (int64_t i = 0; i < N; ++i) s += cs_term((uint64_t)(uint32_t)x[i], i);
+  for (int64_t i = 0; i < N; ++i) s += cs_term((uint64_t)(uint32_t)x[i], off + i);
   return s;
 }
+uint64_t sg_checksum_i32(const int32_t* x, int64_t N) { return sg_checksum_i32_off(x, N, 0); }
 
 uint64_t sg_checksum_bf16(const uint16_t* x, int64_t N) {
   uint64_t s = 0;

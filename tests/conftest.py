@@ -19,7 +19,7 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 device (sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
     # Build in-tree artefacts if missing or stale (no-op when up to date).
-    subprocess.run(["make", "-s", "-C", ROOT, "host"], check=True, stdout=subprocess.DEVNULL)
+    subprocess.run(["make", "-s", "-C", ROOT, "all"], check=True, stdout=subprocess.DEVNULL)
 
 
 @pytest.fixture(scope="session")

@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/mm.h declares, the pure host functions (partition rule, SUMMA panel
+schedule, status strings) behave, and the product path refuses to run without a
+device instead of falling back to the CPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+import paper_2408_15384_b200 as mm
+from paper_2408_15384_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "mm.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mm_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_what_binding_expects():
+    assert declared_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert set(declared_symbols()) <= exported
+    # internal symbols stay hidden (-fvisibility=hidden)
+    assert not any(s.startswith("_ZN3mmb") for s in exported)
+
+
+def test_library_is_sm100a_sass():
+    out = subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for mnemonic in ("UTCHMMA", "UTCIMMA", "UTMALDG", "LDTM", "DMMA"):
+        assert mnemonic in sass, mnemonic
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in mm.version()
+    lib = _lib.load()
+    assert lib.mm_status_string(0) == b"MM_OK"
+    assert lib.mm_status_string(2) == b"MM_ERR_USAGE"
+    assert lib.mm_status_string(99) == b"MM_ERR_UNKNOWN"
+    assert lib.mm_last_error(None) == b"NULL context"
+
+
+def test_null_context_is_usage_error():
+    lib = _lib.load()
+    assert lib.mm_gemm(None, 4, 4, 4, 0, 1, 2, 3, None) == _lib.MM_ERR_USAGE
+    assert lib.mm_sync_check(None, None) == _lib.MM_ERR_USAGE
+    assert lib.mm_create(0, None, 0, None) == _lib.MM_ERR_USAGE
+    lib.mm_destroy(None)  # no-op
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU refusal")
+def test_no_gpu_refuses_instead_of_falling_back():
+    h = ctypes.c_void_p()
+    st = _lib.load().mm_create(0, None, 0, ctypes.byref(h))
+    assert st == _lib.MM_ERR_UNSUPPORTED and not h.value
+    with pytest.raises(mm.MMError):
+        mm.Context(0)
+
+
+# ---------------------------------------------------------------- partition rule
+@pytest.mark.parametrize("total", [1, 2, 7, 8, 9, 100, 16384, 2000])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8, 16])
+def test_shard_range_partition(total, G):
+    q = -(-total // G)
+    covered = []
+    for r in range(G):
+        s, c = mm.shard_range(total, G, r)
+        assert c >= 0
+        if c:
+            covered.extend(range(s, s + c))
+            assert c == q or s + c == total  # all full except the last non-empty one
+    assert covered == list(range(total))  # contiguous, ordered, disjoint, complete
+
+
+def test_shard_range_surplus_workers_empty():
+    assert [mm.shard_range(3, 8, r)[1] for r in range(8)] == [1, 1, 1, 0, 0, 0, 0, 0]
+    assert mm.shard_range(10, 4, 3) == (9, 1)  # ⌈10/4⌉=3: 3,3,3,1
+    assert mm.shard_range(5, 2, 5) == (0, 0)   # r outside [0, G)
+
+
+@pytest.mark.parametrize("n,pr,pc,panel", [(32768, 2, 4, 2048), (1000, 2, 3, 64), (7, 4, 2, 2), (5, 1, 1, 100),
+                                           (1500, 3, 2, 256), (3, 4, 4, 1)])
+def test_summa_panels_cover_and_respect_blocks(n, pr, pc, panel):
+    panels = mm.summa_panels(n, pr, pc, panel)
+    k = 0
+    for (k0, kw, ao, bo) in panels:
+        assert k0 == k and 1 <= kw <= panel
+        s, c = mm.shard_range(n, pc, ao)  # A column block owning the panel
+        assert s <= k0 and k0 + kw <= s + c
+        s, c = mm.shard_range(n, pr, bo)  # B row block owning the panel
+        assert s <= k0 and k0 + kw <= s + c
+        k += kw
+    assert k == n

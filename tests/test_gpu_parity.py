@@ -1,0 +1,357 @@
+"""GPU parity: the CUDA path (through the C-ABI, via the ctypes binding) against
+the CPU oracle, element by element, on seeded inputs (synthgen/).
+
+Bars (BASELINE.json north_star):
+  INT8 -> INT32 : bit-exact.
+  exact-integer FP inputs (any dtype): bit-exact (every partial sum is an
+                  exactly representable integer, so any summation order is exact).
+  FP64 random   : max_ij |C - C_ref| / D_ij <= 1e-12,  D_ij = Σ_k |A_ik B_kj|.
+  BF16 random   : <= 2e-2 (contract) and <= 1e-4 (diagnostic; FP32 accumulation
+                  error is ~1e-7).
+Full config sizes (BASELINE.json configs 0-4) run in the launch configuration
+bench.py times; where the oracle is too slow for the full product, seeded rows
+and columns (plus shard/tile seams) are checked one by one, and the exact-integer
+pins compare the full-output checksum with tests/golden/oracle_fullsize.json
+(written by tools/make_golden.py from the oracle only).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen as sg
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"f64": 1e-12, "bf16": 2e-2}
+DIAG_BF16 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def mm(cuda_device):
+    import paper_2408_15384_b200 as mm_
+    return mm_
+
+
+@pytest.fixture(autouse=True)
+def _clear_cg_env():
+    os.environ.pop("MM_FORCE_CG", None)
+    yield
+    os.environ.pop("MM_FORCE_CG", None)
+
+
+def to_dev(x: np.ndarray, dt: str) -> torch.Tensor:
+    if dt == "bf16":
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_gpu(mm, A, B, dt, cg=None) -> np.ndarray:
+    if cg:
+        os.environ["MM_FORCE_CG"] = str(cg)
+    C = mm.gemm(to_dev(A, dt), to_dev(B, dt))
+    mm.sync_check()
+    return C.cpu().numpy()
+
+
+def gen(dt, kind, seed, m, n, p, K=None):
+    if kind == "exact":
+        if dt == "f64":
+            return sg.exact_f64(seed, 1, K, m, n), sg.exact_f64(seed, 2, K, n, p)
+        if dt == "bf16":
+            return sg.exact_bf16(seed, 1, K, m, n), sg.exact_bf16(seed, 2, K, n, p)
+        return sg.exact_i8(seed, 1, K, m, n), sg.exact_i8(seed, 2, K, n, p)
+    if dt == "f64":
+        return sg.uniform_f64(seed, 1, m, n), sg.uniform_f64(seed, 2, n, p)
+    if dt == "bf16":
+        return sg.normal_bf16(seed, 1, m, n), sg.normal_bf16(seed, 2, n, p)
+    return sg.uniform_i8(seed, 1, m, n), sg.uniform_i8(seed, 2, n, p)
+
+
+def ref(dt, A, B):
+    """(C_ref, D) from the oracle."""
+    if dt == "f64":
+        return oracle.gemm_f64(A, B), oracle.absden_f64(A, B)
+    if dt == "bf16":
+        return oracle.gemm_bf16(A, B)
+    C = oracle.gemm_s8(A, B)
+    return C, None
+
+
+def check(dt, C, Cref, D, exact):
+    if dt == "i8" or exact:
+        assert np.array_equal(np.asarray(C, np.float64), np.asarray(Cref, np.float64)), \
+            f"mismatches: {(np.asarray(C, np.float64) != Cref).sum()}"
+        return 0.0
+    err = oracle.normalized_error(C, Cref, D)
+    assert err <= TOL[dt], err
+    if dt == "bf16":
+        assert err <= DIAG_BF16, f"diagnostic bf16 bound exceeded: {err}"
+    return err
+
+
+# ------------------------------------------------------------------ fixtures (hand-worked)
+with open(os.path.join(GOLDEN, "handworked.json")) as f:
+    HAND = json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", HAND, ids=[c["name"] for c in HAND])
+def test_handworked(mm, case):
+    A = np.asarray(case["A"], np.float64)
+    B = np.asarray(case["B"], np.float64)
+    for dt in case["dtypes"]:
+        dtk = {"s8": "i8"}.get(dt, dt)
+        if dtk == "f64":
+            Ag, Bg = A, B
+        elif dtk == "bf16":
+            Ag = np.vectorize(sg.bf16_from_double, otypes=[np.uint16])(A)
+            Bg = np.vectorize(sg.bf16_from_double, otypes=[np.uint16])(B)
+        else:
+            Ag, Bg = A.astype(np.int8), B.astype(np.int8)
+        for cg in ((1, 2) if dtk != "f64" else (None,)):
+            C = run_gpu(mm, Ag, Bg, dtk, cg)
+            assert np.array_equal(np.asarray(C, np.float64), np.asarray(case["C"], np.float64)), (dtk, cg, C)
+
+
+# ------------------------------------------------------------------ brute force, tiny shapes
+@pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
+def test_all_tiny_shapes_exact(mm, dt):
+    """Every (m,n,p) in {1..8}^3: exact-integer inputs, bit-exact."""
+    K = {"i8": 255, "bf16": 9, "f64": 2049}[dt]
+    for m in range(1, 9):
+        for n in range(1, 9):
+            for p in range(1, 9):
+                seed = 1000 + m * 100 + n * 10 + p
+                A, B = gen(dt, "exact", seed, m, n, p, K)
+                Cref, D = ref(dt, A, B)
+                C = run_gpu(mm, A, B, dt)
+                check(dt, C, Cref, D, exact=True)
+
+
+SEAMS = [1, 15, 16, 17, 63, 64, 65, 127, 128, 129, 255, 256, 257]
+
+
+def _seam_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    return [tuple(int(x) for x in rng.choice(SEAMS, 3)) for _ in range(count)]
+
+
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+@pytest.mark.parametrize("cg", [1, 2])
+def test_tile_seams_tc(mm, dt, cg):
+    for (m, n, p) in _seam_shapes(24, 7 + cg) + [(257, 257, 257), (129, 63, 513), (384, 320, 272)]:
+        A, B = gen(dt, "exact", 77, m, n, p, 255 if dt == "i8" else 9)
+        Cref, D = ref(dt, A, B)
+        C = run_gpu(mm, A, B, dt, cg)
+        check(dt, C, Cref, D, exact=True)
+
+
+def test_tile_seams_f64(mm):
+    for (m, n, p) in _seam_shapes(24, 3) + [(257, 257, 257), (129, 17, 131), (384, 320, 272)]:
+        A, B = gen("f64", "exact", 78, m, n, p, 2049)
+        Cref, D = ref("f64", A, B)
+        check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=True)
+
+
+@pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
+def test_random_values_ragged(mm, dt):
+    for cg in ((1, 2) if dt != "f64" else (None,)):
+        for (m, n, p) in [(300, 200, 520), (129, 1000, 77), (1024, 768, 1280), (5, 4096, 9)]:
+            A, B = gen(dt, "random", 11, m, n, p)
+            Cref, D = ref(dt, A, B)
+            check(dt, run_gpu(mm, A, B, dt, cg), Cref, D, exact=False)
+
+
+# ------------------------------------------------------------------ special cases
+@pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
+def test_identity_zero_transpose(mm, dt):
+    m, n, p = 200, 136, 264
+    A, B = gen(dt, "random", 5, m, n, p)
+    if dt == "bf16":
+        one = sg.bf16_from_double(1.0)
+        I = np.zeros((n, n), np.uint16)
+        np.fill_diagonal(I, one)
+        Z = np.zeros((n, p), np.uint16)
+        Af = sg.bf16_bits_to_f64(A)
+    elif dt == "i8":
+        I = np.eye(n, dtype=np.int8)
+        Z = np.zeros((n, p), np.int8)
+        Af = A.astype(np.float64)
+    else:
+        I = np.eye(n)
+        Z = np.zeros((n, p))
+        Af = A
+    assert np.array_equal(np.asarray(run_gpu(mm, A, I, dt), np.float64), Af)  # A·I = A
+    assert not np.asarray(run_gpu(mm, A, Z, dt), np.float64).any()             # A·0 = 0
+    # (AB)^T = B^T A^T through the library: exact for int8 and exact-int FP
+    Ae, Be = gen(dt, "exact", 6, m, n, p, 255 if dt == "i8" else 9)
+    C1 = run_gpu(mm, Ae, Be, dt)
+    C2 = run_gpu(mm, np.ascontiguousarray(Be.T), np.ascontiguousarray(Ae.T), dt)
+    assert np.array_equal(C1.T, C2)
+
+
+@pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
+def test_misaligned_operands_use_pack_path(mm, dt):
+    """Base pointers off 16-B alignment and odd pitches: padded copy path."""
+    m, n, p = 97, 61, 83  # odd pitches
+    A, B = gen(dt, "exact", 9, m, n, p, 255 if dt == "i8" else 9)
+    Cref, D = ref(dt, A, B)
+    check(dt, run_gpu(mm, A, B, dt), Cref, D, exact=True)
+    # aligned pitch but misaligned base: view into a larger buffer at offset 1 element
+    m, n, p = 64, 64, 64
+    A, B = gen(dt, "exact", 10, m, n, p, 255 if dt == "i8" else 9)
+    Cref, D = ref(dt, A, B)
+    Ad = to_dev(np.concatenate([A.ravel()[:1], A.ravel()]), dt)[1:].view(m, n)
+    Bd = to_dev(np.concatenate([B.ravel()[:1], B.ravel()]), dt)[1:].view(n, p)
+    assert Ad.data_ptr() % 16 != 0
+    C = mm.gemm(Ad, Bd)
+    mm.sync_check()
+    check(dt, C.cpu().numpy(), Cref, D, exact=True)
+
+
+def test_determinism(mm):
+    for dt in ("bf16", "f64", "i8"):
+        A, B = gen(dt, "random", 12, 700, 900, 650)
+        C1 = run_gpu(mm, A, B, dt)
+        C2 = run_gpu(mm, A, B, dt)
+        assert np.array_equal(C1, C2)
+
+
+def test_usage_errors(mm):
+    A = torch.zeros(4, 4, dtype=torch.float64, device="cuda")
+    lib = mm._lib.load()
+    ctx = mm.context(0)
+    assert lib.mm_gemm(ctx.handle, 0, 4, 4, 0, A.data_ptr(), A.data_ptr(), A.data_ptr(), None) == mm._lib.MM_ERR_USAGE
+    assert b"dimensions" in lib.mm_last_error(ctx.handle)
+    assert lib.mm_gemm(ctx.handle, 4, 4, 4, 7, A.data_ptr(), A.data_ptr(), A.data_ptr(), None) == mm._lib.MM_ERR_USAGE
+    assert lib.mm_gemm(ctx.handle, 4, 4, 4, 0, None, A.data_ptr(), A.data_ptr(), None) == mm._lib.MM_ERR_USAGE
+    # C overlapping A
+    assert lib.mm_gemm(ctx.handle, 4, 4, 4, 0, A.data_ptr(), A.data_ptr(), A.data_ptr(), None) == mm._lib.MM_ERR_USAGE
+    assert b"overlaps" in lib.mm_last_error(ctx.handle)
+    with pytest.raises(ValueError):
+        mm.gemm(torch.zeros(3, 4, device="cuda", dtype=torch.float64), torch.zeros(5, 4, device="cuda", dtype=torch.float64))
+    with pytest.raises(TypeError):
+        mm.gemm(torch.zeros(3, 4, device="cuda"), torch.zeros(4, 4, device="cuda"))
+
+
+def test_int32_accumulate_large_k(mm):
+    """INT32 accumulation exact up to n·128² < 2^31: worst-case signs at n = 65536."""
+    m, n, p = 128, 65536, 256
+    A = np.full((m, n), -127, np.int8)
+    B = np.full((n, p), -127, np.int8)
+    A[1] = 127
+    C = run_gpu(mm, A, B, "i8")
+    assert np.all(C[0] == n * 127 * 127) and np.all(C[1] == -n * 127 * 127)
+
+
+def test_host_operand_path(mm):
+    """mm_gemm_host (H2D, product, D2H in overlapped row blocks) equals the oracle."""
+    for dt in ("f64", "bf16", "i8"):
+        m, n, p = 1100, 520, 784
+        A, B = gen(dt, "exact", 13, m, n, p, 255 if dt == "i8" else 9)
+        Cref, D = ref(dt, A, B)
+        if dt == "bf16":
+            At = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).pin_memory()
+            Bt = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).pin_memory()
+        else:
+            At, Bt = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+        C = mm.gemm_host(At, Bt)
+        check(dt, C.numpy(), Cref, D, exact=True)
+
+
+# ------------------------------------------------------------------ BASELINE.json configs, full size
+with open(os.path.join(GOLDEN, "oracle_fullsize.json")) as f:
+    FULL = json.load(f)
+
+
+def _gpu_checksum(C: torch.Tensor, kind: str) -> int:
+    return sg.checksum(C.cpu().numpy(), kind)
+
+
+def test_config0_fp64_256(mm):
+    A, B = gen("f64", "random", 0, 256, 256, 256)
+    Cref, D = ref("f64", A, B)
+    check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=False)
+    A, B = gen("f64", "exact", 0, 256, 256, 256, 2049)
+    C = run_gpu(mm, A, B, "f64")
+    assert sg.checksum(C) == int(FULL["C1x"]["checksum"], 16)
+
+
+def test_config1_fp64_ragged(mm):
+    m, n, p = 2000, 1500, 1750
+    A, B = gen("f64", "random", 1, m, n, p)
+    Cref, D = ref("f64", A, B)
+    check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=False)
+    A, B = gen("f64", "exact", 1, m, n, p, 2049)
+    assert sg.checksum(run_gpu(mm, A, B, "f64")) == int(FULL["C2x"]["checksum"], 16)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_config2_int8_4096(mm, cg):
+    A, B = gen("i8", "random", 2, 4096, 4096, 4096)
+    C = run_gpu(mm, A, B, "i8", cg)
+    assert C.dtype == np.int32
+    assert sg.checksum(C) == int(FULL["C3"]["checksum"], 16)
+    Cref = oracle.gemm_s8(A, B)
+    assert np.array_equal(C.astype(np.int64), Cref)
+
+
+def _sample(n_total, count, role, seed, seams):
+    idx = set(sg.sample_indices(seed, role, count, n_total).tolist())
+    idx |= {i for i in seams if 0 <= i < n_total}
+    return np.array(sorted(idx), np.int64)
+
+
+def test_config3_bf16_16384(mm):
+    N = 16384
+    A, B = gen("bf16", "random", 3, N, N, N)
+    C = run_gpu(mm, A, B, "bf16")
+    seams = [0, N - 1] + [s + d for s in range(0, N, 2048) for d in (-1, 0)] + [255, 256, 257, 8191, 8192]
+    rows = _sample(N, 48, 3, 3, seams)
+    cols = _sample(N, 48, 4, 3, seams)
+    Cr, Dr = oracle.gemm_bf16_rows(A, B, rows)
+    Cc, Dc = oracle.gemm_bf16_cols(A, B, cols)
+    e1 = check("bf16", C[rows], Cr, Dr, exact=False)
+    e2 = check("bf16", C[:, cols], Cc, Dc, exact=False)
+    print(f"C4 bf16 sampled max normalized error: rows {e1:.3e} cols {e2:.3e}")
+
+
+@pytest.mark.parametrize("K", [3, 9])
+def test_config3_bf16_16384_exact_pins(mm, K):
+    key = f"C4x{K}"
+    if key not in FULL:
+        pytest.skip(f"{key} golden not generated yet (tools/make_golden.py)")
+    N = 16384
+    A, B = gen("bf16", "exact", 3, N, N, N, K)
+    Ct = mm.gemm(to_dev(A, "bf16"), to_dev(B, "bf16"))
+    mm.sync_check()
+    C = Ct.cpu().numpy()
+    assert sg.checksum(C) == int(FULL[key]["checksum"], 16)
+    rows = _sample(N, 16, 3, 30 + K, [0, N - 1, 8191, 8192])
+    Cr, _ = oracle.gemm_bf16_rows(A, B, rows)
+    assert np.array_equal(C[rows].astype(np.float64), Cr)
+
+
+def test_config4_fp64_32768_sampled(mm):
+    """configs[4] at full size on one GPU (the SUMMA G=1 reference), oracle on sampled rows/cols."""
+    N = 32768
+    A, B = gen("f64", "random", 4, N, N, N)
+    Ad, Bd = to_dev(A, "f64"), to_dev(B, "f64")
+    C = mm.gemm(Ad, Bd)
+    mm.sync_check()
+    rows = _sample(N, 6, 3, 4, [0, N - 1, 16383, 16384])
+    cols = _sample(N, 6, 4, 4, [0, N - 1, 16383])
+    Crow = C[torch.from_numpy(rows).cuda()].cpu().numpy()
+    Ccol = C[:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    del C, Ad, Bd
+    torch.cuda.empty_cache()
+    Cr, Dr = oracle.gemm_f64_rows(A, B, rows)
+    check("f64", Crow, Cr, Dr, exact=False)
+    Cc, Dc = oracle.gemm_f64_cols(A, B, cols)
+    check("f64", Ccol, Cc, Dc, exact=False)
+    g = json.load(open(os.path.join(GOLDEN, "survey_c6.json")))["C5"]
+    assert Crow[0, 0] == pytest.approx(g["C00"], abs=1e-12 * g["D00"])
