@@ -18,7 +18,8 @@ struct mm_ctx {
   size_t user_ws_bytes = 0;
   void* ws = nullptr;  // internal, grow-only (padding path)
   size_t ws_bytes = 0;
-  int* d_err = nullptr;  // device error word (pipeline timeouts)
+  int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..2] wave-barrier counters
+  int wave_sync = 1;
   // mm_gemm_host staging
   void* hbuf[3] = {nullptr, nullptr, nullptr};
   size_t hbuf_bytes[3] = {0, 0, 0};

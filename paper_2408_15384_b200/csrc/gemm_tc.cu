@@ -141,7 +141,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       bool ok = true;
-      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters) {
+      int j = 0;
+      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters, ++j) {
+        // Wave barrier: start loading tile j only when every CTA has issued all loads of
+        // its tile j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
+        if (args.wave_sync && j > 0 && !counter_wait(args.sync, (unsigned)j * gridDim.x, err, 5)) break;
         int tm, tn;
         sched.tile(t, tm, tn);
         const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
@@ -167,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
+        if (args.wave_sync) red_release_gpu_add(args.sync, 1u);
       }
     }
   } else if (warp == 1) {
@@ -239,6 +244,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<CG>(tmem_base, 512);
+  // the last CTA to finish resets the wave-barrier counters for the next launch
+  if (args.wave_sync && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(args.sync + 1, 1u) == gridDim.x - 1) {
+      atomicExch(args.sync, 0u);
+      atomicExch(args.sync + 1, 0u);
+    }
+  }
 }
 
 template <bool I8, int CG>
@@ -255,8 +268,8 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   TileSched sched;
   sched.tiles_m = (int)((a.M + Cfg::M_MMA - 1) / Cfg::M_MMA);
   sched.tiles_n = (int)((a.N + kBN - 1) / kBN);
-  sched.group_m = 16;
-  if (const char* e = getenv("MM_GROUP_M")) sched.group_m = atoi(e) > 0 ? atoi(e) : 16;  // tuning knob
+  sched.group_m = 8;  // 8 tile-rows x ~9 tile-cols per 74-cluster wave (measured best, tools/sweep_raster.py)
+  if (const char* e = getenv("MM_GROUP_M")) sched.group_m = atoi(e) > 0 ? atoi(e) : 8;  // tuning knob
   if (sched.group_m > sched.tiles_m) sched.group_m = sched.tiles_m;
   const int num_tiles = sched.tiles_m * sched.tiles_n;
   const int num_kb = (int)((a.K + Cfg::BK - 1) / Cfg::BK);

@@ -14,6 +14,8 @@ struct GemmArgs {
   int64_t ldc;
   int beta_one;  // FP64 only: C += A·B (used by SUMMA panels); 0 = overwrite
   int* err;      // device error word (pipeline timeout codes)
+  unsigned* sync;  // [0] wave-barrier arrivals, [1] CTAs done (self-resetting)
+  int wave_sync;   // align the k-phase of all tiles once per wave (L2 reuse)
 };
 
 // BF16 (A,B bf16 -> C f32) and INT8 (A,B s8 -> C s32) on tcgen05.

@@ -155,6 +155,11 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ldc = ldc;
   a.beta_one = beta_one;
   a.err = ctx->d_err;
+  a.sync = reinterpret_cast<unsigned*>(ctx->d_err + 1);
+  // The k-phase barrier pays off only when the operands do not fit in L2 (126 MB):
+  // then the tiles of a wave must walk K together to share A/B slabs.
+  const double operand_bytes = (double)(m * n + n * p) * (double)esz;
+  a.wave_sync = ctx->wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (ctx->wave_sync > 1);
 
   CUtensorMap tmA, tmB;
   uint32_t abox[2], bbox[2];
@@ -256,10 +261,11 @@ __attribute__((visibility("default"))) mm_status mm_create(int device, void* wor
   ctx->cc_minor = prop.minor;
   ctx->user_ws = workspace;
   ctx->user_ws_bytes = workspace ? workspace_bytes : 0;
+  if (const char* e = getenv("MM_WAVE_SYNC")) ctx->wave_sync = atoi(e);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  if (cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->d_err, 4 * sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, 4 * sizeof(int)) != cudaSuccess) {
     cudaSetDevice(prev);
     delete ctx;
     return MM_ERR_RUNTIME;
@@ -302,7 +308,7 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
   if (cudaMemcpy(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "reading the device error word failed");
   if (h != 0) {
-    cudaMemset(ctx->d_err, 0, sizeof(int));
+    cudaMemset(ctx->d_err, 0, 4 * sizeof(int));  // error word + wave-barrier counters
     return set_err(ctx, MM_ERR_RUNTIME, "device pipeline wait timed out (code %d)", h);
   }
   return MM_OK;
