@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "ctx.h"
 #include "kernels.h"
@@ -314,8 +315,13 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
   return MM_OK;
 }
 
-// Host operands: B once, then row blocks of A in / C out on their own streams,
-// so the PCIe copies of block b±1 overlap the product of block b.
+// Host operands.  PCIe, not the tensor cores, bounds this call (C4: 1 GiB in,
+// 1 GiB out vs 7 ms of math), so the copies are scheduled to keep both PCIe
+// directions busy: A arrives in row blocks A_i and B in column panels B_j,
+// interleaved A_0, B_0, A_1, B_1, ... (the computable part of C grows as a
+// square), each block C_ij = A_i·B_j is computed as soon as both have landed
+// and copied back while later blocks are still coming in.  Streams: s_in
+// (H2D), the caller's stream (products), s_out (D2H); events order them.
 __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
                                                               mm_dtype dtype, const void* A, const void* B, void* C,
                                                               void* stream) {
@@ -335,58 +341,87 @@ __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64
   uint8_t* dB = static_cast<uint8_t*>(ctx->hbuf[1]);
   uint8_t* dC = static_cast<uint8_t*>(ctx->hbuf[2]);
   const uint8_t* hA = static_cast<const uint8_t*>(A);
+  const uint8_t* hB = static_cast<const uint8_t*>(B);
   uint8_t* hC = static_cast<uint8_t*>(C);
 
-  // row blocks: ~8 blocks, multiples of 256 rows (one CTA-pair tile height)
-  int64_t rb = round_up((m + 7) / 8, 256);
-  if (rb > m) rb = m;
-  const int64_t nblk = (m + rb - 1) / rb;
-  cudaEvent_t evB, evIn[64], evC[64];
-  if (nblk > 64) rb = round_up((m + 63) / 64, 256);
-  const int64_t nb = (m + rb - 1) / rb;
-  (void)nblk;
-  cudaEventCreateWithFlags(&evB, cudaEventDisableTiming);
-  for (int64_t b = 0; b < nb; ++b) {
-    cudaEventCreateWithFlags(&evIn[b], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&evC[b], cudaEventDisableTiming);
-  }
-  cudaError_t e = cudaSuccess;
-  // the in-stream must not run ahead of earlier work on the caller's stream that reads the buffers
+  // ~8 blocks per axis, multiples of 256 (one CTA-pair tile); small problems: one block.
+  const int64_t small = (int64_t)64 << 20;
+  const bool tiny = (double)(m * n + n * p) * ei < (double)small;
+  int64_t nblk = 4;  // measured best for C4 (tools/e2e_probe.py: 28.6 ms vs 31.5 ms at 8)
+  if (const char* env = getenv("MM_HOST_BLOCKS")) nblk = std::max<int64_t>(1, atoll(env));  // tuning knob
+  const int64_t rb = tiny ? m : std::min(m, round_up((m + nblk - 1) / nblk, 256));
+  const int64_t cb = tiny ? p : std::min(p, round_up((p + nblk - 1) / nblk, 256));
+  const int I = (int)((m + rb - 1) / rb), J = (int)((p + cb - 1) / cb);
+  std::vector<cudaEvent_t> evA(I), evB(J), evC((size_t)I * J);
   cudaEvent_t evStart;
-  cudaEventCreateWithFlags(&evStart, cudaEventDisableTiming);
+  const bool trace = getenv("MM_HOST_TRACE") != nullptr;  // debug: print the copy/compute timeline
+  const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
+  std::vector<cudaEvent_t> evD((size_t)I * J);
+  cudaEventCreateWithFlags(&evStart, evflags);
+  for (auto& e : evA) cudaEventCreateWithFlags(&e, evflags);
+  for (auto& e : evB) cudaEventCreateWithFlags(&e, evflags);
+  for (auto& e : evC) cudaEventCreateWithFlags(&e, evflags);
+  for (auto& e : evD) cudaEventCreateWithFlags(&e, evflags);
+  // copies must not overtake earlier work on the caller's stream that uses the staging buffers
   cudaEventRecord(evStart, s);
   cudaStreamWaitEvent(ctx->s_in, evStart, 0);
   cudaStreamWaitEvent(ctx->s_out, evStart, 0);
-  e = cudaMemcpyAsync(dB, B, (size_t)(n * p) * ei, cudaMemcpyHostToDevice, ctx->s_in);
-  cudaEventRecord(evB, ctx->s_in);
-  for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
-    const int64_t r0 = b * rb, rows = std::min(rb, m - r0);
-    e = cudaMemcpyAsync(dA + r0 * n * ei, hA + r0 * n * ei, (size_t)(rows * n) * ei, cudaMemcpyHostToDevice,
-                        ctx->s_in);
-    cudaEventRecord(evIn[b], ctx->s_in);
-  }
-  cudaStreamWaitEvent(s, evB, 0);
-  for (int64_t b = 0; b < nb && e == cudaSuccess && st == MM_OK; ++b) {
-    const int64_t r0 = b * rb, rows = std::min(rb, m - r0);
-    cudaStreamWaitEvent(s, evIn[b], 0);
-    st = gemm_ld(ctx, rows, n, p, dtype, dA + r0 * n * ei, n, dB, p, dC + r0 * p * eo, p, 0, s);
-    cudaEventRecord(evC[b], s);
-    cudaStreamWaitEvent(ctx->s_out, evC[b], 0);
-    e = cudaMemcpyAsync(hC + r0 * p * eo, dC + r0 * p * eo, (size_t)(rows * p) * eo, cudaMemcpyDeviceToHost,
-                        ctx->s_out);
+
+  cudaError_t e = cudaSuccess;
+  int ia = 0, jb = 0;  // A row blocks / B column panels issued so far
+  auto compute = [&](int i, int j) {
+    const int64_t r0 = (int64_t)i * rb, rows = std::min(rb, m - r0);
+    const int64_t c0 = (int64_t)j * cb, cols = std::min(cb, p - c0);
+    cudaStreamWaitEvent(s, evA[i], 0);
+    cudaStreamWaitEvent(s, evB[j], 0);
+    if (st == MM_OK)
+      st = gemm_ld(ctx, rows, n, cols, dtype, dA + r0 * n * ei, n, dB + c0 * ei, p, dC + (r0 * p + c0) * eo, p, 0, s);
+    cudaEventRecord(evC[(size_t)i * J + j], s);
+    cudaStreamWaitEvent(ctx->s_out, evC[(size_t)i * J + j], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(hC + (r0 * p + c0) * eo, (size_t)p * eo, dC + (r0 * p + c0) * eo, (size_t)p * eo,
+                            (size_t)cols * eo, (size_t)rows, cudaMemcpyDeviceToHost, ctx->s_out);
+    cudaEventRecord(evD[(size_t)i * J + j], ctx->s_out);
+  };
+  while ((ia < I || jb < J) && e == cudaSuccess && st == MM_OK) {
+    const bool takeA = ia < I && (ia <= jb || jb == J);
+    if (takeA) {
+      const int64_t r0 = (int64_t)ia * rb, rows = std::min(rb, m - r0);
+      e = cudaMemcpyAsync(dA + r0 * n * ei, hA + r0 * n * ei, (size_t)(rows * n) * ei, cudaMemcpyHostToDevice,
+                          ctx->s_in);
+      cudaEventRecord(evA[ia], ctx->s_in);
+      for (int j = 0; j < jb; ++j) compute(ia, j);
+      ++ia;
+    } else {
+      const int64_t c0 = (int64_t)jb * cb, cols = std::min(cb, p - c0);
+      e = cudaMemcpy2DAsync(dB + c0 * ei, (size_t)p * ei, hB + c0 * ei, (size_t)p * ei, (size_t)cols * ei, (size_t)n,
+                            cudaMemcpyHostToDevice, ctx->s_in);
+      cudaEventRecord(evB[jb], ctx->s_in);
+      for (int i = 0; i < ia; ++i) compute(i, jb);
+      ++jb;
+    }
   }
   cudaError_t e2 = cudaStreamSynchronize(ctx->s_out);
-  cudaStreamSynchronize(s);
-  cudaEventDestroy(evB);
-  cudaEventDestroy(evStart);
-  for (int64_t b = 0; b < nb; ++b) {
-    cudaEventDestroy(evIn[b]);
-    cudaEventDestroy(evC[b]);
+  cudaError_t e3 = cudaStreamSynchronize(s);
+  cudaStreamSynchronize(ctx->s_in);
+  if (trace) {
+    auto ms = [&](cudaEvent_t ev) { float t = 0; cudaEventElapsedTime(&t, evStart, ev); return t; };
+    for (int i = 0; i < I; ++i) fprintf(stderr, "[mm_gemm_host] A%d in  %8.3f ms\n", i, ms(evA[i]));
+    for (int j = 0; j < J; ++j) fprintf(stderr, "[mm_gemm_host] B%d in  %8.3f ms\n", j, ms(evB[j]));
+    for (int i = 0; i < I; ++i)
+      for (int j = 0; j < J; ++j)
+        fprintf(stderr, "[mm_gemm_host] C%d,%d done %8.3f ms  out %8.3f ms\n", i, j, ms(evC[(size_t)i * J + j]),
+                ms(evD[(size_t)i * J + j]));
   }
+  cudaEventDestroy(evStart);
+  for (auto& x : evD) cudaEventDestroy(x);
+  for (auto& x : evA) cudaEventDestroy(x);
+  for (auto& x : evB) cudaEventDestroy(x);
+  for (auto& x : evC) cudaEventDestroy(x);
   if (st != MM_OK) return st;
-  if (e != cudaSuccess || e2 != cudaSuccess)
+  if (e != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "host pipeline failed: %s",
-                   cudaGetErrorString(e != cudaSuccess ? e : e2));
+                   cudaGetErrorString(e != cudaSuccess ? e : (e2 != cudaSuccess ? e2 : e3)));
   return mm_sync_check(ctx, s);
 }
 

@@ -1,0 +1,95 @@
+"""mm_gemm_sharded through NCCL on the one GPU this round has (world size 1):
+the row-block path with MM_BCAST_B | MM_GATHER_C and the SUMMA 1×1 path run the
+real NCCL calls (broadcast, grouped send/recv, comm split) and must equal the
+oracle bit-exactly on exact-integer inputs.  Multi-rank schedules are covered on
+CPU by tests/test_dist_gloo.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen as sg
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def pg(cuda_device):
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_row_block_world1(pg):
+    import paper_2408_15384_b200 as mm
+    m, n, p = 1000, 768, 520
+    for dt, gen in (("bf16", sg.exact_bf16), ("i8", sg.exact_i8), ("f64", sg.exact_f64)):
+        K = {"bf16": 9, "i8": 255, "f64": 2049}[dt]
+        A, B = gen(31, 1, K, m, n), gen(31, 2, K, n, p)
+        if dt == "bf16":
+            tA = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).cuda()
+            tB = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).cuda()
+            Cref, _ = oracle.gemm_bf16(A, B)
+            tdt, odt = torch.bfloat16, torch.float32
+        elif dt == "i8":
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_s8(A, B)
+            tdt, odt = torch.int8, torch.int32
+        else:
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_f64(A, B)
+            tdt, odt = torch.float64, torch.float64
+        C_loc = torch.empty(m, p, dtype=odt, device="cuda")
+        C_full = torch.zeros(m, p, dtype=odt, device="cuda")
+        mm.gemm_sharded(m, n, p, tdt, tA, tB, C_loc, layout=mm.MM_ROW_BLOCK,
+                        flags=mm.MM_BCAST_B | mm.MM_GATHER_C, root=0, C_full=C_full)
+        mm.sync_check()
+        assert np.array_equal(C_loc.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
+        assert np.array_equal(C_full.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
+
+
+@pytest.mark.parametrize("panel", ["64", "2048"])
+def test_summa_world1_fp64(pg, panel):
+    import paper_2408_15384_b200 as mm
+    os.environ["MM_SUMMA_PANEL"] = panel
+    try:
+        m, n, p = 700, 1000, 900
+        A, B = sg.exact_f64(32, 1, 2049, m, n), sg.exact_f64(32, 2, 2049, n, p)
+        C = torch.empty(m, p, dtype=torch.float64, device="cuda")
+        mm.gemm_sharded(m, n, p, torch.float64, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), C,
+                        layout=mm.MM_SUMMA_2D, grid=(1, 1))
+        mm.sync_check()
+        assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
+        # random values: panels accumulate with beta=1, within the FP64 tolerance
+        A, B = sg.uniform_f64(33, 1, m, n), sg.uniform_f64(33, 2, n, p)
+        mm.gemm_sharded(m, n, p, torch.float64, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), C,
+                        layout=mm.MM_SUMMA_2D, grid=(1, 1))
+        mm.sync_check()
+        err = oracle.normalized_error(C.cpu().numpy(), oracle.gemm_f64(A, B), oracle.absden_f64(A, B))
+        assert err <= 1e-12, err
+    finally:
+        os.environ.pop("MM_SUMMA_PANEL", None)
+
+
+def test_sharded_usage_errors(pg):
+    import paper_2408_15384_b200 as mm
+    t = torch.zeros(4, 4, dtype=torch.float64, device="cuda")
+    with pytest.raises(mm.MMError, match="grid"):
+        mm.gemm_sharded(4, 4, 4, torch.float64, t, t.clone(), t.clone(), layout=mm.MM_SUMMA_2D, grid=(2, 1))
+    with pytest.raises(mm.MMError, match="root"):
+        mm.gemm_sharded(4, 4, 4, torch.float64, t, t.clone(), t.clone(), layout=mm.MM_ROW_BLOCK, root=3)
