@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmm_b200.so")
+LIB_PATH = os.environ.get("MM_B200_LIB") or os.path.join(_HERE, "libmm_b200.so")  # override: A/B builds
 
 MM_F64, MM_BF16_F32, MM_S8_S32 = 0, 1, 2
 MM_OK, MM_ERR_RUNTIME, MM_ERR_USAGE, MM_ERR_UNSUPPORTED, MM_ERR_WORKSPACE = 0, 1, 2, 3, 4

@@ -31,6 +31,10 @@ struct mm_ctx {
   void* col_comm = nullptr;
   void* split_parent = nullptr;
   int split_rows = 0, split_cols = 0;
+  void* sk_ws = nullptr;  // stream-K partial tiles (both kernels)
+  size_t sk_ws_bytes = 0;
+  unsigned* sk_flags = nullptr;  // stream-K per-tile counters (self-resetting)
+  size_t sk_flag_count = 0;
   uint64_t launches = 0;  // kernels launched by this context
   std::string last_error;
 };

@@ -8,13 +8,22 @@
 // producer warp and eight consumer warps ("cache tiling",
 // PAPER.md:366-373 prefetching/pipelining, done by TMA instead of the CPU).
 //
-// CTA tile 128×128, K slab 16 (one 128-B swizzle row of A).  Consumer warp w
-// owns a 64×32 sub-tile (2×4 warp grid): 8×4 DMMA tiles, 64 accumulators.
+// Work split: "stream-K".  The (tile, k-block) iteration space is cut into
+// gridDim.x equal contiguous ranges, one per persistent CTA, so every SM gets
+// the same number of DMMA k-blocks whatever the tile count (no partial last
+// wave: C2's 224 tiles on 148 SMs, C1's 16 small tiles).  A tile whose k-range
+// spans several CTAs is finished by the CTA holding its k-block 0 (always the
+// last segment of that CTA's range): the other contributors (whose segment is
+// the first of their range) publish partial tiles to a workspace and bump a
+// per-tile counter; the finisher adds them in CTA order — a fixed order, so
+// results are deterministic run to run.
+//
+// CTA tile BM×BN (128×128, or 64×64 for small problems), K slab 16 (one 128-B
+// swizzle row of A).  Consumer warp w owns a (BM/2)×(BN/4) sub-tile.
 // Fragment loads are conflict-free with the swizzle because each DMMA's four
 // k indices are taken from rows {b, b+1, b+4, b+5} of the slab (b ∈ {0,2,8,10}):
 // the same four k's for A and B, so each DMMA still adds A[i][k]·B[k][j] over
-// its four k's; only which k's are grouped together changes (the sum over all
-// k is unchanged up to FP64 rounding order).
+// its four k's; only which k's are grouped together changes.
 // Edges: TMA zero-fills out-of-bounds reads; stores are predicated.
 #include "kernels.h"
 #include "ptx.cuh"
@@ -23,33 +32,55 @@ namespace mmb {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int BK = 16;
 constexpr int STAGES = 6;
-constexpr int A_BYTES = BM * BK * 8;        // 16 KB, one box {16, 128}
-constexpr int BBOX_BYTES = BK * 16 * 8;      // 2 KB, box {16 cols, 16 rows}
-constexpr int NBBOX = BN / 16;               // 8 boxes
-constexpr int B_BYTES = NBBOX * BBOX_BYTES;  // 16 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NCONS = 8;                      // consumer warps
-constexpr int kThreads = (NCONS + 1) * 32;    // + producer warp
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
+constexpr int BBOX_BYTES = BK * 16 * 8;  // 2 KB, box {16 cols, 16 rows}
+constexpr int NCONS = 8;                  // consumer warps
+constexpr int kThreads = (NCONS + 1) * 32;
 
+template <int BM, int BN>
+struct F64Cfg {
+  static constexpr int A_BYTES = BM * BK * 8;  // one box {16, BM}
+  static constexpr int NBBOX = BN / 16;
+  static constexpr int B_BYTES = NBBOX * BBOX_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
+  static constexpr int MI = BM / 16;  // 8-row DMMA tiles per warp (warp rows = BM/2)
+  static constexpr int NI = BN / 32;  // 8-col DMMA tiles per warp (warp cols = BN/4)
+};
+
+__device__ __forceinline__ int64_t range_start(int c, int64_t total, int G) { return ((int64_t)c * total) / G; }
+
+__device__ __forceinline__ int cta_of(int64_t it, int64_t total, int G) {
+  int c = (int)((it * G) / total);
+  while (c + 1 < G && range_start(c + 1, total, G) <= it) ++c;
+  while (c > 0 && range_start(c, total, G) > it) --c;
+  return c;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int BM, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
-                    int tiles_m, int tiles_n, int num_kb) {
+                    int tiles_m, int num_kb, int64_t total_iters) {
+  using Cfg = F64Cfg<BM, BN>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw_u32);
   const uint32_t sA = base;
-  const uint32_t sB = base + STAGES * A_BYTES;
-  const uint32_t bar0 = smem_u32(smem + STAGES * STAGE_BYTES);
+  const uint32_t sB = base + STAGES * Cfg::A_BYTES;
+  const uint32_t bar0 = smem_u32(smem + STAGES * Cfg::STAGE_BYTES);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int num_tiles = tiles_m * tiles_n;
+  const int G = gridDim.x;
+  const int c = blockIdx.x;
+  const int64_t it_begin = range_start(c, total_iters, G);
+  const int64_t it_end = range_start(c + 1, total_iters, G);
   int* err = args.err;
 
   if (warp == NCONS && lane == 0) {
@@ -68,133 +99,190 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      bool ok = true;
-      for (int t = blockIdx.x; t < num_tiles && ok; t += gridDim.x) {
+      for (int64_t it = it_begin; it < it_end; ++it) {
+        const int t = (int)(it / num_kb), kb = (int)(it - (int64_t)t * num_kb);
         const int tm = t % tiles_m, tn = t / tiles_m;  // M fastest: neighbours share B columns
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) { ok = false; break; }
-          mbar_arrive_expect_tx(full_bar(stage), STAGE_BYTES);
-          const int k0 = kb * BK;
-          tma_load_2d(sA + stage * A_BYTES, &tmA, full_bar(stage), k0, m0);
+        if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) break;
+        mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+        const int k0 = kb * BK;
+        tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, full_bar(stage), k0, tm * BM);
 #pragma unroll
-          for (int b = 0; b < NBBOX; ++b)
-            tma_load_2d(sB + stage * B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), n0 + b * 16, k0);
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-        }
+        for (int b = 0; b < Cfg::NBBOX; ++b)
+          tma_load_2d(sB + stage * Cfg::B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), tn * BN + b * 16, k0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
     }
   } else {
     // ---------------------------------------------------------------- DMMA consumers
-    const int wm = (int)warp >> 2;  // 0..1 : rows wm*64
-    const int wn = (int)warp & 3;   // 0..3 : cols wn*32
+    const int wm = (int)warp >> 2;  // 0..1 : rows wm*(BM/2)
+    const int wn = (int)warp & 3;   // 0..3 : cols wn*(BN/4)
     const int g = (int)lane >> 2;   // fragment row / column index 0..7
     const int kk = (int)lane & 3;   // fragment k index 0..3
     const int kofs = (kk & 1) + ((kk >> 1) << 2);  // k within quad: {0,1,4,5}
-    // Per-lane smem byte offsets (stage-relative), for quad base 0; quad b adds to k.
-    int a_row[8];
-#pragma unroll
-    for (int mi = 0; mi < 8; ++mi) a_row[mi] = wm * 64 + mi * 8 + g;
-    int b_col[4];
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b_col[ni] = wn * 32 + ni * 8 + g;
-
     double* C = reinterpret_cast<double*>(args.C);
+    double* part = reinterpret_cast<double*>(args.ws);
     const bool vec_ok = ((args.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     int stage = 0;
     uint32_t phase = 0;
     bool ok = true;
-    for (int t = blockIdx.x; t < num_tiles && ok; t += gridDim.x) {
+    int64_t it = it_begin;
+    while (it < it_end && ok) {
+      const int t = (int)(it / num_kb);
+      const int kb0 = (int)(it - (int64_t)t * num_kb);
+      const int64_t kb_end = (int64_t)kb0 + (it_end - it);
+      const int kb1 = kb_end < (int64_t)num_kb ? (int)kb_end : num_kb;
       const int tm = t % tiles_m, tn = t / tiles_m;
-      double acc[8][4][2];
+      double acc[Cfg::MI][Cfg::NI][2];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < Cfg::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         if (!mbar_wait(full_bar(stage), phase, err, 12)) { ok = false; break; }
-        const uint8_t* pa = smem + stage * A_BYTES;
-        const uint8_t* pb = smem + STAGES * A_BYTES + stage * B_BYTES;
+        const uint8_t* pa = smem + stage * Cfg::A_BYTES;
+        const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES;
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
           const int k = ((qd & 1) << 1) + ((qd >> 1) << 3) + kofs;  // quad bases 0,2,8,10
-          double af[8], bf[4];
+          double af[Cfg::MI], bf[Cfg::NI];
 #pragma unroll
-          for (int mi = 0; mi < 8; ++mi) {
-            const int r = a_row[mi];
-            af[mi] = *reinterpret_cast<const double*>(pa + r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3));
+          for (int mi = 0; mi < Cfg::MI; ++mi) {
+            const int r = wm * (BM / 2) + mi * 8 + g;
+            af[mi] = *reinterpret_cast<const double*>(pa + r * 128 + (((k >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3));
           }
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
-            const int c = b_col[ni];
-            const int cc = c & 15;
-            bf[ni] = *reinterpret_cast<const double*>(pb + (c >> 4) * BBOX_BYTES + k * 128 +
-                                                      ((((cc >> 1) ^ (k & 7))) << 4) + ((cc & 1) << 3));
+          for (int ni = 0; ni < Cfg::NI; ++ni) {
+            const int cc = wn * (BN / 4) + ni * 8 + g;
+            const int c16 = cc & 15;
+            bf[ni] = *reinterpret_cast<const double*>(pb + (cc >> 4) * BBOX_BYTES + k * 128 +
+                                                      (((c16 >> 1) ^ (k & 7)) << 4) + ((c16 & 1) << 3));
           }
 #pragma unroll
-          for (int mi = 0; mi < 8; ++mi)
+          for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+            for (int ni = 0; ni < Cfg::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_bar(stage));
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
       if (!ok) break;
-      // epilogue: registers -> global (predicated on the ragged edges)
+
+      const bool whole = (kb0 == 0 && kb1 == num_kb);
+      if (!whole && kb0 != 0) {
+        // ---- contributor: publish the partial tile, then signal the finisher
+        double* slot = part + (size_t)c * (BM * BN);
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + g;
-        if (row >= args.M) continue;
+        for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int64_t col = (int64_t)tn * BN + wn * 32 + ni * 8 + kk * 2;
-          double* dst = C + row * args.ldc + col;
-          double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
-          if (vec_ok && col + 1 < args.N) {
-            if (args.beta_one) {
-              const double2 o = *reinterpret_cast<const double2*>(dst);
-              v0 += o.x;
-              v1 += o.y;
+          for (int ni = 0; ni < Cfg::NI; ++ni) {
+            const int r = wm * (BM / 2) + mi * 8 + g, cc = wn * (BN / 4) + ni * 8 + kk * 2;
+            __stcg(reinterpret_cast<double2*>(slot + r * BN + cc), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+          }
+        __threadfence();
+        named_bar(1, NCONS * 32);
+        if (warp == 0 && lane == 0) red_release_gpu_add(args.flags + t, 1u);
+      } else {
+        if (!whole) {
+          // ---- finisher (holds k-block 0): wait for the other contributors, add them in CTA order
+          const int c_last = cta_of((int64_t)t * num_kb + num_kb - 1, total_iters, G);
+          const unsigned expect = (unsigned)(c_last - c);
+          if (warp == 0 && lane == 0) {
+            if (!counter_wait(args.flags + t, expect, err, 13)) ok = false;
+            else *(volatile unsigned*)(args.flags + t) = 0u;  // reset for the next launch
+          }
+          named_bar(1, NCONS * 32);
+          for (int q = c + 1; q <= c_last; ++q) {
+            const double* slot = part + (size_t)q * (BM * BN);
+#pragma unroll
+            for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < Cfg::NI; ++ni) {
+                const int r = wm * (BM / 2) + mi * 8 + g, cc = wn * (BN / 4) + ni * 8 + kk * 2;
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(slot + r * BN + cc));
+                acc[mi][ni][0] += v.x;
+                acc[mi][ni][1] += v.y;
+              }
+          }
+        }
+        // ---- epilogue: registers -> global (predicated on the ragged edges), β ∈ {0, 1}
+#pragma unroll
+        for (int mi = 0; mi < Cfg::MI; ++mi) {
+          const int64_t row = (int64_t)tm * BM + wm * (BM / 2) + mi * 8 + g;
+          if (row >= args.M) continue;
+#pragma unroll
+          for (int ni = 0; ni < Cfg::NI; ++ni) {
+            const int64_t col = (int64_t)tn * BN + wn * (BN / 4) + ni * 8 + kk * 2;
+            double* dst = C + row * args.ldc + col;
+            double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
+            if (vec_ok && col + 1 < args.N) {
+              if (args.beta_one) {
+                const double2 o = *reinterpret_cast<const double2*>(dst);
+                v0 += o.x;
+                v1 += o.y;
+              }
+              *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+            } else {
+              if (col < args.N) dst[0] = args.beta_one ? dst[0] + v0 : v0;
+              if (col + 1 < args.N) dst[1] = args.beta_one ? dst[1] + v1 : v1;
             }
-            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-          } else {
-            if (col < args.N) dst[0] = args.beta_one ? dst[0] + v0 : v0;
-            if (col + 1 < args.N) dst[1] = args.beta_one ? dst[1] + v1 : v1;
           }
         }
       }
+      it += kb1 - kb0;
     }
   }
   __syncwarp();
   __syncthreads();
 }
 
+template <int BM, int BN>
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
+                        cudaStream_t s) {
+  using Cfg = F64Cfg<BM, BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_f64_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  gemm_f64_kernel<BM, BN><<<pl.grid, kThreads, Cfg::SMEM_BYTES, s>>>(tmA, tmB, a, pl.tiles_m, pl.num_kb,
+                                                                      (int64_t)pl.tiles_m * pl.tiles_n * pl.num_kb);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
-void f64_box_dims(uint32_t* a_box, uint32_t* b_box) {
+F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
+  F64Plan pl;
+  const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
+  pl.bm = pl.bn = (t128 >= num_sms) ? 128 : 64;
+  pl.tiles_m = (int)((M + pl.bm - 1) / pl.bm);
+  pl.tiles_n = (int)((N + pl.bn - 1) / pl.bn);
+  pl.num_kb = (int)((K + BK - 1) / BK);
+  const int64_t total = (int64_t)pl.tiles_m * pl.tiles_n * pl.num_kb;
+  // each CTA should own >= 4 k-blocks (pipeline fill) and every tile has at most ~4 contributors
+  int64_t g = std::min<int64_t>((int64_t)num_sms, (total + 3) / 4);
+  g = std::min<int64_t>(g, (int64_t)pl.tiles_m * pl.tiles_n * 4);
+  pl.grid = (int)std::max<int64_t>(1, g);
+  pl.ws_bytes = (size_t)pl.grid * pl.bm * pl.bn * sizeof(double);
+  pl.flag_count = pl.tiles_m * pl.tiles_n;
+  return pl;
+}
+
+void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
   a_box[0] = BK;
-  a_box[1] = BM;
+  a_box[1] = (uint32_t)pl.bm;
   b_box[0] = 16;
   b_box[1] = BK;
 }
 
-cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int num_sms,
+cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                             cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int tiles_m = (int)((a.M + BM - 1) / BM);
-  const int tiles_n = (int)((a.N + BN - 1) / BN);
-  const int num_tiles = tiles_m * tiles_n;
-  const int num_kb = (int)((a.K + BK - 1) / BK);
-  int grid = num_tiles < num_sms ? num_tiles : num_sms;
-  gemm_f64_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(tmA, tmB, a, tiles_m, tiles_n, num_kb);
-  return cudaGetLastError();
+  if (pl.bm == 128) return launch_impl<128, 128>(tmA, tmB, a, pl, s);
+  return launch_impl<64, 64>(tmA, tmB, a, pl, s);
 }
 
 }  // namespace mmb

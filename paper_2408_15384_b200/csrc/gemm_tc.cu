@@ -22,6 +22,7 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> global).
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -49,7 +50,8 @@ struct TcCfg {
   static constexpr int B_BYTES = NBOX * BOX_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (CG == 1) ? 4 : 6;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr int M_MMA = 128 * CG;
   // Instruction descriptor: c_format [4,6), a_format [7,10), b_format [10,13),
   // a_major [15] = K, b_major [16] = MN, N>>3 at [17,23), M>>4 at [24,29).
@@ -57,9 +59,22 @@ struct TcCfg {
                                     ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(M_MMA >> 4) << 24);
 };
 
-struct TileSched {
-  int tiles_m, tiles_n, group_m;
-  __device__ __forceinline__ void tile(int t, int& tm, int& tn) const {
+// Work schedule: every cluster first takes whole tiles round-robin (W full waves,
+// grouped raster), then the tiles of the last, partial wave are split stream-K
+// style: their (tile, k-block) iterations are cut into ntc equal ranges, one per
+// cluster, so no SM idles through a ragged last wave (C3: 3.46 waves -> 3 + an
+// even tail; C4: 55.35 -> 55 + tail).  A split tile is finished by the cluster
+// holding its k-block 0 (the last segment of that cluster's range); the others
+// (the first segment of theirs) publish partial tiles and bump a counter; the
+// finisher adds them in cluster order (fixed order: deterministic).
+struct WorkSched {
+  int tiles_m, tiles_n, group_m, num_kb;
+  int nc;    // clusters
+  int W;     // full data-parallel waves
+  int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
+  int64_t TI;  // tail iterations = tail tiles * num_kb
+
+  __device__ __forceinline__ void tile_coords(int t, int& tm, int& tn) const {
     const int per_group = group_m * tiles_n;
     const int g = t / per_group;
     const int first_m = g * group_m;
@@ -67,6 +82,38 @@ struct TileSched {
     const int r = t - g * per_group;
     tm = first_m + r % gm;
     tn = r / gm;
+  }
+  __device__ __forceinline__ int64_t tstart(int c) const { return ((int64_t)c * TI) / ntc; }
+  __device__ __forceinline__ int tail_cluster_of(int64_t it) const {
+    int c = (int)((it * ntc) / TI);
+    while (c + 1 < ntc && tstart(c + 1) <= it) ++c;
+    while (c > 0 && tstart(c) > it) --c;
+    return c;
+  }
+  // j-th work item of cluster c: tile t, k-blocks [kb0, kb1). Returns false past the end.
+  __device__ __forceinline__ bool item(int c, int j, int& t, int& kb0, int& kb1) const {
+    if (j < W) {
+      t = c + j * nc;
+      kb0 = 0;
+      kb1 = num_kb;
+      return t < tiles_m * tiles_n;
+    }
+    if (c >= ntc) return false;
+    int64_t it = tstart(c);
+    const int64_t end = tstart(c + 1);
+    for (int s = 0; it < end; ++s) {
+      const int64_t tt = it / num_kb;
+      const int k0 = (int)(it - tt * num_kb);
+      const int64_t lim = (tt + 1) * num_kb < end ? (tt + 1) * num_kb : end;
+      if (s == j - W) {
+        t = W * nc + (int)tt;
+        kb0 = k0;
+        kb1 = (int)(lim - tt * num_kb);
+        return true;
+      }
+      it = lim;
+    }
+    return false;
   }
 };
 
@@ -88,10 +135,28 @@ __device__ __forceinline__ void store_row32(uint32_t* __restrict__ C, int64_t ld
   }
 }
 
+// Partial slabs are stored "row-interleaved": uint4 element (chunk c, vector i, row r) at
+// (c*8 + i)*128 + r, so a warp's 32 rows form one contiguous 512-B request (coalesced).
+template <bool I8>
+__device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict__ src /* = slab + c*8*128 + row */) {
+  uint4 w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 128);  // 8 independent loads in flight
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t x[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if constexpr (I8) v[4 * i + u] = (uint32_t)((int32_t)v[4 * i + u] + (int32_t)x[u]);
+      else v[4 * i + u] = __float_as_uint(__uint_as_float(v[4 * i + u]) + __uint_as_float(x[u]));
+    }
+  }
+}
+
 template <bool I8, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
-                   TileSched sched, int num_kb) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
   using Cfg = TcCfg<I8, CG>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment (SWIZZLE_128B atoms) of the operand ring.
@@ -100,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + (base - raw_u32);
   const uint32_t sA = base;
   const uint32_t sB = base + Cfg::STAGES * Cfg::A_BYTES;
-  uint8_t* bar_area = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  const uint32_t sEpi = base + Cfg::STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (SWIZZLE_128B staging)
+  uint8_t* bar_area = smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES;
   const uint32_t bar0 = smem_u32(bar_area);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (Cfg::STAGES + s); };
@@ -111,14 +177,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
-  const int cluster_idx = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
-  const int num_clusters = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
-  const int num_tiles = sched.tiles_m * sched.tiles_n;
+  const int cl = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int num_kb = sched.num_kb;
   int* err = args.err;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (args.c_tma) tma_prefetch_desc(&tmC);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
@@ -141,16 +207,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       bool ok = true;
-      int j = 0;
-      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters, ++j) {
-        // Wave barrier: start loading tile j only when every CTA has issued all loads of
-        // its tile j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
-        if (args.wave_sync && j > 0 && !counter_wait(args.sync, (unsigned)j * gridDim.x, err, 5)) break;
+      int t, kb0, kb1;
+      for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
+        // Wave barrier: start item j only when every CTA has issued all loads of its
+        // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
+        if (args.wave_sync && j > 0 && j <= sched.W &&
+            !counter_wait(args.sync, (unsigned)j * gridDim.x, err, 5))
+          break;
         int tm, tn;
-        sched.tile(t, tm, tn);
+        sched.tile_coords(t, tm, tn);
         const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = tn * kBN + (int)rank * Cfg::BN_CTA;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
           const uint32_t sb = sB + stage * Cfg::B_BYTES;
@@ -171,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
-        if (args.wave_sync) red_release_gpu_add(args.sync, 1u);
+        if (args.wave_sync && j < sched.W) red_release_gpu_add(args.sync, 1u);
       }
     }
   } else if (warp == 1) {
@@ -179,16 +247,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (rank == 0 && lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int j = 0;
       bool ok = true;
-      for (int t = cluster_idx; t < num_tiles && ok; t += num_clusters, ++j) {
+      int t, kb0, kb1;
+      for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         const int acc = j & 1;
         const uint32_t use = (uint32_t)(j >> 1);
         if (!(CG == 2 ? mbar_wait_cluster(tempty_bar(acc), (use & 1u) ^ 1u, err, 2)
                       : mbar_wait(tempty_bar(acc), (use & 1u) ^ 1u, err, 2))) { ok = false; break; }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kBN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (!mbar_wait(full_bar(stage), phase, err, 3)) { ok = false; break; }
           tc_fence_after();
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
@@ -199,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
             // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
             const uint64_t bdesc = umma_desc_sw128(sb + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-            tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC, (kb | kk) != 0 ? 1u : 0u);
+            tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
           tc_commit<CG>(empty_bar(stage));  // frees this smem stage (both CTAs) when the MMAs retire
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
@@ -212,23 +280,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
     uint32_t* C = reinterpret_cast<uint32_t*>(args.C);
+    uint32_t* part = reinterpret_cast<uint32_t*>(args.ws);
     const bool vec_ok = ((args.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
-    int j = 0;
-    for (int t = cluster_idx; t < num_tiles; t += num_clusters, ++j) {
+    const int prow = (int)(q * 32 + lane);  // row of this thread inside the CTA's 128-row slab
+    // C tile chunk (32 rows x 32 columns) -> global: through a 128B-swizzled smem buffer and one
+    // TMA store (coalesced full lines, edges clipped by the tensor map), or, when C's base/pitch
+    // rule out TMA, straight from registers with predicated stores.
+    uint32_t n_stores = 0;
+    auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0) {
+      if (args.c_tma) {
+        const uint32_t buf = sEpi + ((q * 2u + (n_stores & 1u)) * 4096u);
+        if (n_stores >= 2) {
+          if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
+          __syncwarp();
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
+                       v[4 * i + 2], v[4 * i + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)row_base);
+          bulk_commit();
+        }
+        ++n_stores;
+      } else {
+        store_row32(C, args.ldc, row_base + lane, col0, args.M, args.N, v, vec_ok);
+      }
+    };
+    int t, kb0, kb1;
+    for (int j = 0; sched.item(cl, j, t, kb0, kb1); ++j) {
       int tm, tn;
-      sched.tile(t, tm, tn);
+      sched.tile_coords(t, tm, tn);
       const int acc = j & 1;
       const uint32_t use = (uint32_t)(j >> 1);
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       tc_fence_after();
-      const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + q * 32 + lane;
+      const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * kBN);
+      const bool whole = (kb0 == 0 && kb1 == num_kb);
+      const int tail_c = cl;  // tail items: cluster index == tail-slot index
+      const int64_t row_base = row - lane;  // first row of this warp's 32-row block
+      if (whole) {
 #pragma unroll 1
-      for (int c = 0; c < kBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + c * 32, v);
-        tmem_ld_wait();
-        store_row32(C, args.ldc, row, (int64_t)tn * kBN + c * 32, args.M, args.N, v, vec_ok);
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+          emit(v, row_base, (int64_t)tn * kBN + c * 32);
+        }
+      } else if (kb0 != 0) {
+        // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
+        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * kBN)) + prow;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            __stcg(slot + (c * 8 + i) * 128, make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * CG + rank, 1u);
+      } else {
+        // finisher (holds k-block 0): wait for the contributors, add their slabs in cluster order
+        const int64_t ti_last = (int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1;
+        const int c_last = sched.tail_cluster_of(ti_last);
+        if (q == 0 && lane == 0) {
+          if (counter_wait(args.flags + (size_t)t * CG + rank, (unsigned)(c_last - tail_c), err, 6))
+            *(volatile unsigned*)(args.flags + (size_t)t * CG + rank) = 0u;  // reset for the next launch
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+          for (int qq = tail_c + 1; qq <= c_last; ++qq)
+            add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * kBN)) + c * 8 * 128 + prow);
+          emit(v, row_base, (int64_t)tn * kBN + c * 32);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -237,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mbar_arrive(tempty_bar(acc));
       }
     }
+    if (args.c_tma && lane == 0) bulk_wait<0>();  // all output stores complete before exit
   }
 
   __syncwarp();
@@ -254,9 +389,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+WorkSched make_sched(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_sms) {
+  const int m_mma = 128 * cg;
+  const int bk = i8 ? 128 : 64;
+  WorkSched s;
+  s.tiles_m = (int)((M + m_mma - 1) / m_mma);
+  s.tiles_n = (int)((N + kBN - 1) / kBN);
+  s.group_m = 8;  // 8 tile-rows x ~9 tile-cols per 74-cluster wave (measured best, tools/sweep_raster.py)
+  if (const char* e = getenv("MM_GROUP_M")) s.group_m = atoi(e) > 0 ? atoi(e) : 8;  // tuning knob
+  if (s.group_m > s.tiles_m) s.group_m = s.tiles_m;
+  s.num_kb = (int)((K + bk - 1) / bk);
+  const int64_t T = (int64_t)s.tiles_m * s.tiles_n;
+  int64_t nc = num_sms / cg;
+  nc = std::min<int64_t>(nc, T * 4);  // at most ~4 clusters share one tile
+  s.nc = (int)std::max<int64_t>(1, nc);
+  s.W = (int)(T / s.nc);
+  const int64_t tail = T - (int64_t)s.W * s.nc;
+  s.TI = tail * s.num_kb;
+  // The split tail pays for its partial-slab round trip only when there are many full waves
+  // (measured: C4 55 waves +0.6 %, C3 3 waves -12 %; tools/ab_gpu.py).
+  bool split = tail > 0 && s.W >= 8;
+  if (const char* e = getenv("MM_STREAMK")) split = tail > 0 && atoi(e) != 0;  // tuning knob
+  if (!split) {
+    // no stream-K tail: the last partial wave runs whole tiles
+    s.W = (int)((T + s.nc - 1) / s.nc);
+    s.ntc = 0;
+    s.TI = 0;
+  } else {
+    // >= 4 k-blocks per segment, <= 4 segments per tile
+    int64_t ntc = std::min<int64_t>(s.nc, tail * 4);
+    ntc = std::min<int64_t>(ntc, std::max<int64_t>(1, s.TI / 4));
+    s.ntc = (int)std::max<int64_t>(1, ntc);
+  }
+  return s;
+}
+
 template <bool I8, int CG>
-cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int num_sms,
-                        cudaStream_t s) {
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
+                        int num_sms, cudaStream_t s) {
   using Cfg = TcCfg<I8, CG>;
   auto kern = gemm_tc_kernel<I8, CG>;
   static bool attr_set = false;  // per template instance
@@ -265,20 +435,9 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  TileSched sched;
-  sched.tiles_m = (int)((a.M + Cfg::M_MMA - 1) / Cfg::M_MMA);
-  sched.tiles_n = (int)((a.N + kBN - 1) / kBN);
-  sched.group_m = 8;  // 8 tile-rows x ~9 tile-cols per 74-cluster wave (measured best, tools/sweep_raster.py)
-  if (const char* e = getenv("MM_GROUP_M")) sched.group_m = atoi(e) > 0 ? atoi(e) : 8;  // tuning knob
-  if (sched.group_m > sched.tiles_m) sched.group_m = sched.tiles_m;
-  const int num_tiles = sched.tiles_m * sched.tiles_n;
-  const int num_kb = (int)((a.K + Cfg::BK - 1) / Cfg::BK);
-  int clusters = num_sms / CG;
-  if (clusters > num_tiles) clusters = num_tiles;
-  if (clusters < 1) clusters = 1;
-
+  const WorkSched sched = make_sched(I8, CG, a.M, a.N, a.K, num_sms);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CG, 1, 1);
+  cfg.gridDim = dim3(sched.nc * CG, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = s;
@@ -289,7 +448,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a, sched, num_kb);
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, a, sched);
 }
 
 }  // namespace
@@ -303,10 +462,19 @@ void tc_box_dims(bool i8, int cg, uint32_t* a_box, uint32_t* b_box) {
   (void)cg;
 }
 
-cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
-                           int num_sms, cudaStream_t s) {
-  if (i8) return cg == 2 ? launch_impl<true, 2>(tmA, tmB, a, num_sms, s) : launch_impl<true, 1>(tmA, tmB, a, num_sms, s);
-  return cg == 2 ? launch_impl<false, 2>(tmA, tmB, a, num_sms, s) : launch_impl<false, 1>(tmA, tmB, a, num_sms, s);
+void tc_plan_needs(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
+                   size_t* flag_count) {
+  const WorkSched sc = make_sched(i8, cg, M, N, K, num_sms);
+  *ws_bytes = (size_t)sc.ntc * cg * 128 * kBN * 4;
+  *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg;
+}
+
+cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                           const GemmArgs& a, int num_sms, cudaStream_t s) {
+  if (i8)
+    return cg == 2 ? launch_impl<true, 2>(tmA, tmB, tmC, a, num_sms, s) : launch_impl<true, 1>(tmA, tmB, tmC, a, num_sms, s);
+  return cg == 2 ? launch_impl<false, 2>(tmA, tmB, tmC, a, num_sms, s)
+                 : launch_impl<false, 1>(tmA, tmB, tmC, a, num_sms, s);
 }
 
 }  // namespace mmb

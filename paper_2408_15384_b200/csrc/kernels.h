@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 namespace mmb {
@@ -16,19 +17,33 @@ struct GemmArgs {
   int* err;      // device error word (pipeline timeout codes)
   unsigned* sync;  // [0] wave-barrier arrivals, [1] CTAs done (self-resetting)
   int wave_sync;   // align the k-phase of all tiles once per wave (L2 reuse)
+  void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
+  unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
+  int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
 };
+
+// FP64 launch plan (tile shape, stream-K grid, workspace needs).
+struct F64Plan {
+  int bm, bn, tiles_m, tiles_n, num_kb, grid;
+  size_t ws_bytes;
+  int flag_count;
+};
+F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms);
 
 // BF16 (A,B bf16 -> C f32) and INT8 (A,B s8 -> C s32) on tcgen05.
 // tmA: dims {K, M} box {128 B of K, 128 rows}; tmB: dims {N, K} box {128 B of N, BK rows}; both SWIZZLE_128B.
-cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
-                           int num_sms, cudaStream_t s);
+cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                           const GemmArgs& a, int num_sms, cudaStream_t s);
+// Workspace (stream-K partial slabs) and per-tile counters the launch will use.
+void tc_plan_needs(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
+                   size_t* flag_count);
 // Box extents the tensor maps must be encoded with.
 void tc_box_dims(bool i8, int cg, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
 
 // FP64 on DMMA (mma.sync m8n8k4) with TMA-fed smem ring.
-cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, int num_sms,
+cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                             cudaStream_t s);
-void f64_box_dims(uint32_t* a_box, uint32_t* b_box);
+void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box);
 
 // Copy a rows×cols matrix (pitch src_ld elements) into dst (pitch dst_ld >= cols), zero-filling
 // columns [cols, dst_ld).  esize ∈ {1, 2, 8}.  Coalesced 16-byte stores on the destination.

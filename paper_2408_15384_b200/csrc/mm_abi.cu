@@ -165,25 +165,68 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   CUtensorMap tmA, tmB;
   uint32_t abox[2], bbox[2];
   cudaError_t e;
+  a.ws = nullptr;
+  a.flags = nullptr;
+  a.c_tma = 0;
+  // stream-K workspace (partial tiles) + self-resetting per-tile counters, shared by both kernels
+  auto ensure_sk = [&](size_t ws_bytes, size_t flag_count) -> mm_status {
+    if (ctx->sk_flag_count < flag_count) {
+      if (ctx->sk_flags) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->sk_flags);
+        ctx->sk_flags = nullptr;
+        ctx->sk_flag_count = 0;
+      }
+      if (cudaMalloc(&ctx->sk_flags, flag_count * sizeof(unsigned)) != cudaSuccess ||
+          cudaMemset(ctx->sk_flags, 0, flag_count * sizeof(unsigned)) != cudaSuccess)
+        return set_err(ctx, MM_ERR_WORKSPACE, "stream-K counter allocation failed");
+      ctx->sk_flag_count = flag_count;
+    }
+    if (ws_bytes) {
+      mm_status wst = ensure_buffer(ctx, &ctx->sk_ws, &ctx->sk_ws_bytes, ws_bytes);
+      if (wst != MM_OK) return wst;
+    }
+    a.ws = ctx->sk_ws;
+    a.flags = ctx->sk_flags;
+    return MM_OK;
+  };
   if (dtype == MM_F64) {
-    f64_box_dims(abox, bbox);
-    mm_status st = encode_2d(ctx, &tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Ause, m, n, padA ? ldA2 : lda, abox, "A");
+    const F64Plan pl = f64_plan(m, p, n, ctx->num_sms);
+    mm_status st = ensure_sk(pl.ws_bytes, (size_t)pl.flag_count);
+    if (st != MM_OK) return st;
+    f64_box_dims(pl, abox, bbox);
+    st = encode_2d(ctx, &tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Ause, m, n, padA ? ldA2 : lda, abox, "A");
     if (st != MM_OK) return st;
     st = encode_2d(ctx, &tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
-    e = launch_gemm_f64(tmA, tmB, a, ctx->num_sms, s);
+    e = launch_gemm_f64(tmA, tmB, a, pl, s);
   } else {
     if (beta_one) return set_err(ctx, MM_ERR_UNSUPPORTED, "accumulate (beta=1) is only implemented for MM_F64");
     const bool i8 = dtype == MM_S8_S32;
     int cg = force_cg();
     if (!cg) cg = (m <= 128) ? 1 : 2;
+    size_t ws_bytes = 0, flag_count = 0;
+    tc_plan_needs(i8, cg, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
+    mm_status st = ensure_sk(ws_bytes, flag_count);
+    if (st != MM_OK) return st;
     tc_box_dims(i8, cg, abox, bbox);
     const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    mm_status st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
+    st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
     if (st != MM_OK) return st;
     st = encode_2d(ctx, &tmB, dt, esz, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
-    e = launch_gemm_tc(i8, cg, tmA, tmB, a, ctx->num_sms, s);
+    // C through TMA stores when its base and pitch allow (else predicated register stores)
+    CUtensorMap tmC;
+    memset(&tmC, 0, sizeof tmC);
+    a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
+    if (const char* env = getenv("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
+    if (a.c_tma) {
+      const uint32_t cbox[2] = {32, 32};
+      st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
+                     cbox, "C");
+      if (st != MM_OK) return st;
+    }
+    e = launch_gemm_tc(i8, cg, tmA, tmB, tmC, a, ctx->num_sms, s);
   }
   if (e == cudaSuccess) ++ctx->launches;
   if (e != cudaSuccess) {
@@ -283,6 +326,8 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   cudaDeviceSynchronize();
   mm_release_comms(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->sk_ws) cudaFree(ctx->sk_ws);
+  if (ctx->sk_flags) cudaFree(ctx->sk_flags);
   for (auto& b : ctx->hbuf)
     if (b) cudaFree(b);
   for (auto& b : ctx->sbuf)
@@ -310,6 +355,7 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
     return set_err(ctx, MM_ERR_RUNTIME, "reading the device error word failed");
   if (h != 0) {
     cudaMemset(ctx->d_err, 0, 4 * sizeof(int));  // error word + wave-barrier counters
+    if (ctx->sk_flags) cudaMemset(ctx->sk_flags, 0, ctx->sk_flag_count * sizeof(unsigned));
     return set_err(ctx, MM_ERR_RUNTIME, "device pipeline wait timed out (code %d)", h);
   }
   return MM_OK;
