@@ -208,6 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       bool ok = true;
       int t, kb0, kb1;
+      // L2 priorities (large operands): the A panels of a raster group are re-read by every
+      // wave of the group, the B slabs only within one wave -> keep A, stream B.
+      // l2_hint bit 0: A evict_last; bit 1: B evict_first (else evict_normal)
+      const uint64_t pol_a = (args.l2_hint & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const uint64_t pol_b = (args.l2_hint & 2) ? l2_policy_evict_first() : l2_policy_evict_normal();
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         // Wave barrier: start item j only when every CTA has issued all loads of its
         // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
@@ -225,17 +230,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * Cfg::BK;
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, full_bar(stage), k0, m0);
+            if (args.l2_hint) {
+              tma_load_2d_hint(sa, &tmA, full_bar(stage), k0, m0, pol_a);
 #pragma unroll
-            for (int b = 0; b < Cfg::NBOX; ++b)
-              tma_load_2d(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0);
+              for (int b = 0; b < Cfg::NBOX; ++b)
+                tma_load_2d_hint(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0, pol_b);
+            } else {
+              tma_load_2d(sa, &tmA, full_bar(stage), k0, m0);
+#pragma unroll
+              for (int b = 0; b < Cfg::NBOX; ++b)
+                tma_load_2d(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0);
+            }
           } else {
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
-            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+            if (args.l2_hint) {
+              tma_load_2d_pair_hint(sa, &tmA, leader_full, k0, m0, pol_a);
 #pragma unroll
-            for (int b = 0; b < Cfg::NBOX; ++b)
-              tma_load_2d_pair(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0);
+              for (int b = 0; b < Cfg::NBOX; ++b)
+                tma_load_2d_pair_hint(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0, pol_b);
+            } else {
+              tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+#pragma unroll
+              for (int b = 0; b < Cfg::NBOX; ++b)
+                tma_load_2d_pair(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0);
+            }
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }

@@ -20,6 +20,7 @@ struct GemmArgs {
   void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
+  int l2_hint;      // tcgen05 kernel: TMA loads of A evict_last, of B evict_first
 };
 
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).

@@ -168,6 +168,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ws = nullptr;
   a.flags = nullptr;
   a.c_tma = 0;
+  // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
+  // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
+  a.l2_hint = 0;
+  if (const char* env = getenv("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
   // stream-K workspace (partial tiles) + self-resetting per-tile counters, shared by both kernels
   auto ensure_sk = [&](size_t ws_bytes, size_t flag_count) -> mm_status {
     if (ctx->sk_flag_count < flag_count) {
