@@ -35,21 +35,24 @@ namespace {
 constexpr int kThreads = 192;
 constexpr int kBN = 256;  // MMA N (columns of C per tile)
 
-template <bool I8, int CG>
+template <bool I8, int CG, int NT>
 struct TcCfg {
   static constexpr int ESZ = I8 ? 1 : 2;
   static constexpr int BK = 128 / ESZ;        // K elements per stage (one 128-B swizzle atom)
   static constexpr int UK = I8 ? 32 : 16;     // K per tcgen05.mma
   static constexpr int KSTEPS = BK / UK;      // 4
   static constexpr int BM = 128;              // rows of A per CTA
-  static constexpr int BN_CTA = kBN / CG;     // columns of B per CTA
+  static constexpr int TILE_N = kBN * NT;     // columns of C per tile (NT accumulators of N=256)
+  static constexpr int NBUF = (NT == 1) ? 2 : 1;  // TMEM accumulator buffers: NBUF * TILE_N = 512 columns
+  static constexpr int BN_CTA = kBN / CG;     // columns of B per CTA per MMA region
   static constexpr int BOXN = 128 / ESZ;      // columns per TMA box of B (128 B)
-  static constexpr int NBOX = BN_CTA / BOXN;
+  static constexpr int NBOX = BN_CTA / BOXN;  // boxes per region
   static constexpr int A_BYTES = BM * 128;
   static constexpr int BOX_BYTES = BK * 128;
-  static constexpr int B_BYTES = NBOX * BOX_BYTES;
+  static constexpr int REGION_BYTES = NBOX * BOX_BYTES;
+  static constexpr int B_BYTES = NT * REGION_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 1) ? 4 : 6;
+  static constexpr int STAGES = (CG == 1 || NT == 2) ? 4 : 6;
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr int M_MMA = 128 * CG;
@@ -153,11 +156,11 @@ __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict
   }
 }
 
-template <bool I8, int CG>
+template <bool I8, int CG, int NT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
-  using Cfg = TcCfg<I8, CG>;
+  using Cfg = TcCfg<I8, CG, NT>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment (SWIZZLE_128B atoms) of the operand ring.
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < Cfg::NBUF; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 4 * CG);
     }
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tm, tn;
         sched.tile_coords(t, tm, tn);
         const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
-        const int n0 = tn * kBN + (int)rank * Cfg::BN_CTA;
+        const int n0 = tn * Cfg::TILE_N + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
         for (int kb = kb0; kb < kb1; ++kb) {
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
@@ -233,13 +236,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (args.l2_hint) {
               tma_load_2d_hint(sa, &tmA, full_bar(stage), k0, m0, pol_a);
 #pragma unroll
-              for (int b = 0; b < Cfg::NBOX; ++b)
-                tma_load_2d_hint(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0, pol_b);
+              for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
+                tma_load_2d_hint(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
+                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
             } else {
               tma_load_2d(sa, &tmA, full_bar(stage), k0, m0);
 #pragma unroll
-              for (int b = 0; b < Cfg::NBOX; ++b)
-                tma_load_2d(sb + b * Cfg::BOX_BYTES, &tmB, full_bar(stage), n0 + b * Cfg::BOXN, k0);
+              for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
+                tma_load_2d(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
+                            n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0);
             }
           } else {
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
@@ -247,13 +252,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (args.l2_hint) {
               tma_load_2d_pair_hint(sa, &tmA, leader_full, k0, m0, pol_a);
 #pragma unroll
-              for (int b = 0; b < Cfg::NBOX; ++b)
-                tma_load_2d_pair_hint(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0, pol_b);
+              for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
+                tma_load_2d_pair_hint(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
+                                      n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
             } else {
               tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
 #pragma unroll
-              for (int b = 0; b < Cfg::NBOX; ++b)
-                tma_load_2d_pair(sb + b * Cfg::BOX_BYTES, &tmB, leader_full, n0 + b * Cfg::BOXN, k0);
+              for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
+                tma_load_2d_pair(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
+                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0);
             }
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
@@ -269,12 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool ok = true;
       int t, kb0, kb1;
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
-        const int acc = j & 1;
-        const uint32_t use = (uint32_t)(j >> 1);
+        const int acc = j % Cfg::NBUF;
+        const uint32_t use = (uint32_t)(j / Cfg::NBUF);
         if (!(CG == 2 ? mbar_wait_cluster(tempty_bar(acc), (use & 1u) ^ 1u, err, 2)
                       : mbar_wait(tempty_bar(acc), (use & 1u) ^ 1u, err, 2))) { ok = false; break; }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kBN);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * Cfg::TILE_N);
         for (int kb = kb0; kb < kb1; ++kb) {
           if (!mbar_wait(full_bar(stage), phase, err, 3)) { ok = false; break; }
           tc_fence_after();
@@ -284,9 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
             // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); K step = 32 B.
             const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
-            // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
-            const uint64_t bdesc = umma_desc_sw128(sb + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-            tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC, (kb != kb0 || kk != 0) ? 1u : 0u);
+#pragma unroll
+            for (int rr = 0; rr < NT; ++rr) {
+              // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
+              const uint64_t bdesc =
+                  umma_desc_sw128(sb + rr * Cfg::REGION_BYTES + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
+              tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (kb != kb0 || kk != 0) ? 1u : 0u);
+            }
           }
           tc_commit<CG>(empty_bar(stage));  // frees this smem stage (both CTAs) when the MMAs retire
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
@@ -332,28 +343,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; sched.item(cl, j, t, kb0, kb1); ++j) {
       int tm, tn;
       sched.tile_coords(t, tm, tn);
-      const int acc = j & 1;
-      const uint32_t use = (uint32_t)(j >> 1);
+      const int acc = j % Cfg::NBUF;
+      const uint32_t use = (uint32_t)(j / Cfg::NBUF);
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       tc_fence_after();
       const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + prow;
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * kBN);
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
       const bool whole = (kb0 == 0 && kb1 == num_kb);
       const int tail_c = cl;  // tail items: cluster index == tail-slot index
       const int64_t row_base = row - lane;  // first row of this warp's 32-row block
       if (whole) {
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
-          emit(v, row_base, (int64_t)tn * kBN + c * 32);
+          emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
         }
       } else if (kb0 != 0) {
         // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
-        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * kBN)) + prow;
+        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * Cfg::TILE_N)) + prow;
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
@@ -374,13 +385,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
           for (int qq = tail_c + 1; qq <= c_last; ++qq)
-            add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * kBN)) + c * 8 * 128 + prow);
-          emit(v, row_base, (int64_t)tn * kBN + c * 32);
+            add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * Cfg::TILE_N)) + c * 8 * 128 + prow);
+          emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
         }
       }
       tc_fence_before();
@@ -408,14 +419,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-WorkSched make_sched(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_sms) {
+WorkSched make_sched(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, int num_sms) {
   const int m_mma = 128 * cg;
   const int bk = i8 ? 128 : 64;
   WorkSched s;
   s.tiles_m = (int)((M + m_mma - 1) / m_mma);
-  s.tiles_n = (int)((N + kBN - 1) / kBN);
-  s.group_m = 8;  // 8 tile-rows x ~9 tile-cols per 74-cluster wave (measured best, tools/sweep_raster.py)
-  if (const char* e = getenv("MM_GROUP_M")) s.group_m = atoi(e) > 0 ? atoi(e) : 8;  // tuning knob
+  s.tiles_n = (int)((N + kBN * nt - 1) / (kBN * nt));
+  // measured best (tools/sweep_raster.py): 256-wide tiles 8 tile-rows x ~9 tile-cols per 74-cluster wave;
+  // 512-wide tiles 16 x ~4.6
+  s.group_m = nt == 2 ? 16 : 8;
+  if (const char* e = getenv("MM_GROUP_M")) s.group_m = atoi(e) > 0 ? atoi(e) : s.group_m;  // tuning knob
   if (s.group_m > s.tiles_m) s.group_m = s.tiles_m;
   s.num_kb = (int)((K + bk - 1) / bk);
   const int64_t T = (int64_t)s.tiles_m * s.tiles_n;
@@ -443,18 +456,18 @@ WorkSched make_sched(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_s
   return s;
 }
 
-template <bool I8, int CG>
+template <bool I8, int CG, int NT>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
                         int num_sms, cudaStream_t s) {
-  using Cfg = TcCfg<I8, CG>;
-  auto kern = gemm_tc_kernel<I8, CG>;
+  using Cfg = TcCfg<I8, CG, NT>;
+  auto kern = gemm_tc_kernel<I8, CG, NT>;
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const WorkSched sched = make_sched(I8, CG, a.M, a.N, a.K, num_sms);
+  const WorkSched sched = make_sched(I8, CG, NT, a.M, a.N, a.K, num_sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sched.nc * CG, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -481,19 +494,23 @@ void tc_box_dims(bool i8, int cg, uint32_t* a_box, uint32_t* b_box) {
   (void)cg;
 }
 
-void tc_plan_needs(bool i8, int cg, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
+void tc_plan_needs(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
                    size_t* flag_count) {
-  const WorkSched sc = make_sched(i8, cg, M, N, K, num_sms);
-  *ws_bytes = (size_t)sc.ntc * cg * 128 * kBN * 4;
+  const WorkSched sc = make_sched(i8, cg, nt, M, N, K, num_sms);
+  *ws_bytes = (size_t)sc.ntc * cg * 128 * kBN * nt * 4;
   *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg;
 }
 
-cudaError_t launch_gemm_tc(bool i8, int cg, const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                           const GemmArgs& a, int num_sms, cudaStream_t s) {
-  if (i8)
-    return cg == 2 ? launch_impl<true, 2>(tmA, tmB, tmC, a, num_sms, s) : launch_impl<true, 1>(tmA, tmB, tmC, a, num_sms, s);
-  return cg == 2 ? launch_impl<false, 2>(tmA, tmB, tmC, a, num_sms, s)
-                 : launch_impl<false, 1>(tmA, tmB, tmC, a, num_sms, s);
+cudaError_t launch_gemm_tc(bool i8, int cg, int nt, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s) {
+  if (i8) {
+    if (cg == 1) return launch_impl<true, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+    return nt == 2 ? launch_impl<true, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
+                   : launch_impl<true, 2, 1>(tmA, tmB, tmC, a, num_sms, s);
+  }
+  if (cg == 1) return launch_impl<false, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+  return nt == 2 ? launch_impl<false, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
+                 : launch_impl<false, 2, 1>(tmA, tmB, tmC, a, num_sms, s);
 }
 
 }  // namespace mmb
