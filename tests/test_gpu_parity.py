@@ -173,6 +173,23 @@ def test_stream_k_split_tiles(mm, dt, cg):
         check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=False)
 
 
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+@pytest.mark.parametrize("streamk", ["0", "1"])
+def test_wide_tiles_nt2(mm, dt, streamk):
+    """512-wide CTA-pair tiles (two TMEM accumulators), forced on small/ragged shapes,
+    with and without the stream-K split tail."""
+    os.environ["MM_NT"] = "2"
+    os.environ["MM_STREAMK"] = streamk
+    try:
+        for (m, n, p) in [(300, 200, 520), (512, 4096, 1024), (1100, 768, 1700), (256, 64, 2048), (2048, 1024, 4608)]:
+            A, B = gen(dt, "exact", 43, m, n, p, 255 if dt == "i8" else 9)
+            Cref, D = ref(dt, A, B)
+            check(dt, run_gpu(mm, A, B, dt, 2), Cref, D, exact=True)
+    finally:
+        os.environ.pop("MM_NT", None)
+        os.environ.pop("MM_STREAMK", None)
+
+
 @pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
 def test_random_values_ragged(mm, dt):
     for cg in ((1, 2) if dt != "f64" else (None,)):
