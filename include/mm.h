@@ -102,7 +102,14 @@ const char* mm_last_error(const mm_ctx* ctx);
  *   flags: MM_BCAST_B — B is valid only on `root` and is broadcast first
  *          (B_local must be an n×p buffer on every rank);
  *          MM_GATHER_C — after the product, the full m×p C is assembled on
- *          `root` into C_full (ignored elsewhere).
+ *          `root` into C_full (ignored elsewhere) by NCCL send/recv;
+ *          MM_GATHER_C_FUSED — the same result without a separate gather:
+ *          every rank's product kernel stores its C tiles straight into the
+ *          root's C_full over NVLink (peer memory, CUDA IPC mapping of the
+ *          root's allocation exchanged through the communicator), so the
+ *          transfer overlaps the math tile by tile; C_local is not written
+ *          (may be NULL).  Ends with a communicator-wide barrier so C_full is
+ *          complete on `root` when the call's stream work finishes.
  * MM_SUMMA_2D: ranks form a grid_rows × grid_cols grid (G = grid_rows*grid_cols),
  *   rank r ↔ (r / grid_cols, r % grid_cols).  Rank (i,j) owns block (i,j)
  *   of A (row block i of m, column block j of n), of B (row block i of n,
@@ -115,7 +122,7 @@ const char* mm_last_error(const mm_ctx* ctx);
  * time from the libnccl.so.2 already loaded in the process.
  */
 typedef enum { MM_ROW_BLOCK = 0, MM_SUMMA_2D = 1 } mm_layout;
-enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u };
+enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u, MM_GATHER_C_FUSED = 4u };
 
 mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                           mm_layout layout, int grid_rows, int grid_cols,

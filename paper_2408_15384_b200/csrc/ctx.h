@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "mm.h"
 
@@ -35,6 +37,9 @@ struct mm_ctx {
   size_t sk_ws_bytes = 0;
   unsigned* sk_flags = nullptr;  // stream-K per-tile counters (self-resetting)
   size_t sk_flag_count = 0;
+  void* ipc_xchg = nullptr;  // device staging for the IPC handle exchange (fused gather)
+  std::vector<std::pair<std::string, void*>> ipc_open;  // opened peer allocations (handle bytes -> base)
+  void* bar_buf = nullptr;   // one int for the communicator barrier
   uint64_t launches = 0;  // kernels launched by this context
   std::string last_error;
 };

@@ -6,7 +6,11 @@
 //
 //   MM_ROW_BLOCK — rank r owns a contiguous block of rows of A and C
 //     (mm_shard_range, SPEC.md:210 ⌈m/G⌉ rule); B is replicated
-//     (optionally broadcast from `root` first); C optionally gathered.
+//     (optionally broadcast from `root` first); C optionally gathered —
+//     by NCCL send/recv after the product (MM_GATHER_C), or fused into the
+//     product (MM_GATHER_C_FUSED): each rank's tcgen05/DMMA kernel stores its C
+//     tiles straight into the root's C_full through a CUDA-IPC peer mapping
+//     (TMA stores over NVLink), so the gather overlaps the math tile by tile.
 //     No exchange is needed for the product itself.
 //   MM_SUMMA_2D — ranks form a grid; for each k-panel the owner column of
 //     A broadcasts its panel along its grid row and the owner row of B along
@@ -21,6 +25,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstring>
+#include <string>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -35,6 +41,7 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
@@ -59,6 +66,7 @@ const NcclApi& nccl() {
     LOAD(Broadcast, "ncclBroadcast");
     LOAD(Send, "ncclSend");
     LOAD(Recv, "ncclRecv");
+    LOAD(AllReduce, "ncclAllReduce");
     LOAD(GroupStart, "ncclGroupStart");
     LOAD(GroupEnd, "ncclGroupEnd");
     LOAD(CommSplit, "ncclCommSplit");
@@ -67,7 +75,7 @@ const NcclApi& nccl() {
     LOAD(CommUserRank, "ncclCommUserRank");
     LOAD(GetErrorString, "ncclGetErrorString");
 #undef LOAD
-    g_nccl.ok = g_nccl.Broadcast && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
+    g_nccl.ok = g_nccl.Broadcast && g_nccl.AllReduce && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
                 g_nccl.CommSplit && g_nccl.CommCount && g_nccl.CommUserRank && g_nccl.GetErrorString;
   });
   return g_nccl;
@@ -83,6 +91,71 @@ const NcclApi& nccl() {
 struct Range {
   int64_t start, count;
 };
+
+// cuMemGetAddressRange from the driver (base + size of the allocation holding a pointer).
+typedef CUresult (*GetAddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+GetAddrRangeFn addr_range_fn() {
+  static GetAddrRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (GetAddrRangeFn) nullptr;
+    }
+    return reinterpret_cast<GetAddrRangeFn>(f);
+  }();
+  return fn;
+}
+
+// Collective: every rank learns a pointer to the root's `root_ptr` it can store to
+// (the root's own pointer on the root; a CUDA-IPC mapping of the root's allocation,
+// over NVLink, elsewhere).  The 64-byte IPC handle + offset travel by ncclBroadcast.
+mm_status peer_pointer_of_root(mm_ctx* ctx, void* root_ptr, int root, int r, ncclComm_t comm, cudaStream_t s,
+                               uint8_t** out) {
+  struct Msg {
+    cudaIpcMemHandle_t h;
+    uint64_t offset;
+  } msg;
+  memset(&msg, 0, sizeof msg);
+  if (r == root) {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    GetAddrRangeFn fn = addr_range_fn();
+    if (!fn || fn(&base, &size, reinterpret_cast<CUdeviceptr>(root_ptr)) != CUDA_SUCCESS)
+      return set_err(ctx, MM_ERR_RUNTIME, "cuMemGetAddressRange failed for C_full");
+    if (cudaIpcGetMemHandle(&msg.h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(ctx, MM_ERR_RUNTIME, "cudaIpcGetMemHandle failed for C_full");
+    }
+    msg.offset = reinterpret_cast<uint64_t>(root_ptr) - (uint64_t)base;
+  }
+  if (!ctx->ipc_xchg && cudaMalloc(&ctx->ipc_xchg, 256) != cudaSuccess)
+    return set_err(ctx, MM_ERR_WORKSPACE, "IPC exchange buffer allocation failed");
+  if (r == root && cudaMemcpyAsync(ctx->ipc_xchg, &msg, sizeof msg, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "IPC handle staging failed");
+  NCCL_CHECK(ctx, nccl().Broadcast(ctx->ipc_xchg, ctx->ipc_xchg, sizeof msg, ncclUint8, root, comm, s));
+  if (cudaMemcpyAsync(&msg, ctx->ipc_xchg, sizeof msg, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "IPC handle exchange failed");
+  if (r == root) {
+    *out = static_cast<uint8_t*>(root_ptr);
+    return MM_OK;
+  }
+  const std::string key(reinterpret_cast<const char*>(&msg.h), sizeof msg.h);
+  void* base = nullptr;
+  for (auto& kv : ctx->ipc_open)
+    if (kv.first == key) base = kv.second;
+  if (!base) {
+    if (cudaIpcOpenMemHandle(&base, msg.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(ctx, MM_ERR_RUNTIME, "cudaIpcOpenMemHandle of the root's C_full failed (peer access?)");
+    }
+    ctx->ipc_open.emplace_back(key, base);
+  }
+  *out = static_cast<uint8_t*>(base) + msg.offset;
+  return MM_OK;
+}
 Range shard(int64_t total, int G, int r) {
   Range x;
   mm_shard_range(total, G, r, &x.start, &x.count);
@@ -145,6 +218,11 @@ __attribute__((visibility("default"))) int mm_summa_panels(int64_t n, int grid_r
 
 void mm_release_comms(mm_ctx* ctx) {
   if (!ctx) return;
+  for (auto& kv : ctx->ipc_open) cudaIpcCloseMemHandle(kv.second);
+  ctx->ipc_open.clear();
+  if (ctx->ipc_xchg) cudaFree(ctx->ipc_xchg);
+  if (ctx->bar_buf) cudaFree(ctx->bar_buf);
+  ctx->ipc_xchg = ctx->bar_buf = nullptr;
   const NcclApi& api = nccl();
   if (api.CommDestroy) {
     if (ctx->row_comm) api.CommDestroy(static_cast<ncclComm_t>(ctx->row_comm));
@@ -162,6 +240,23 @@ static mm_status row_block(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtyp
   const Range mine = shard(m, G, r);
   if (flags & MM_BCAST_B)
     NCCL_CHECK(ctx, api.Broadcast(B_local, B_local, (size_t)(n * p) * ei, ncclUint8, root, comm, s));
+  if (flags & MM_GATHER_C_FUSED) {
+    // GEMM -> gather as ONE kernel per rank: the epilogue's TMA stores target the root's
+    // C_full (peer memory over NVLink), rows [row0, row0+rows).
+    if (r == root && !C_full) return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C_FUSED needs C_full on the root rank");
+    uint8_t* target = nullptr;
+    mm_status st = peer_pointer_of_root(ctx, C_full, root, r, comm, s, &target);
+    if (st != MM_OK) return st;
+    if (mine.count > 0) {
+      st = gemm_ld(ctx, mine.count, n, p, dtype, A_local, n, B_local, p, target + mine.start * p * eo, p, 0, s);
+      if (st != MM_OK) return st;
+    }
+    // barrier: the root's C_full is complete once every rank's product kernel has finished
+    if (!ctx->bar_buf && cudaMalloc(&ctx->bar_buf, 16) != cudaSuccess)
+      return set_err(ctx, MM_ERR_WORKSPACE, "barrier buffer allocation failed");
+    NCCL_CHECK(ctx, api.AllReduce(ctx->bar_buf, ctx->bar_buf, 1, ncclInt32, ncclSum, comm, s));
+    return MM_OK;
+  }
   if (mine.count > 0) {
     mm_status st = gemm_ld(ctx, mine.count, n, p, dtype, A_local, n, B_local, p, C_local, p, 0, s);
     if (st != MM_OK) return st;
@@ -316,7 +411,8 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
     if (root < 0 || root >= G) return set_err(ctx, MM_ERR_USAGE, "root %d outside [0, %d)", root, G);
     if (!B_local) return set_err(ctx, MM_ERR_USAGE, "B_local is NULL");
     const Range mine = shard(m, G, r);
-    if (mine.count > 0 && (!A_local || !C_local)) return set_err(ctx, MM_ERR_USAGE, "NULL A_local/C_local");
+    if (mine.count > 0 && (!A_local || (!C_local && !(flags & MM_GATHER_C_FUSED))))
+      return set_err(ctx, MM_ERR_USAGE, "NULL A_local/C_local");
     return row_block(ctx, m, n, p, dtype, A_local, B_local, C_local, C_full, flags, root, comm, G, r, s);
   }
   if (layout == MM_SUMMA_2D) {

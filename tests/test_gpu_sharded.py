@@ -63,6 +63,37 @@ def test_row_block_world1(pg):
         assert np.array_equal(C_full.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
 
 
+def test_row_block_fused_gather_world1(pg):
+    """MM_GATHER_C_FUSED: the product kernel stores straight into the root's C_full
+    (at world size 1 the root maps its own buffer; the IPC open path needs >= 2 GPUs)."""
+    import paper_2408_15384_b200 as mm
+    m, n, p = 1000, 512, 776
+    for dt in ("bf16", "i8", "f64"):
+        if dt == "bf16":
+            A, B = sg.exact_bf16(34, 1, 9, m, n), sg.exact_bf16(34, 2, 9, n, p)
+            tA = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).cuda()
+            tB = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).cuda()
+            Cref, _ = oracle.gemm_bf16(A, B)
+            tdt, odt = torch.bfloat16, torch.float32
+        elif dt == "i8":
+            A, B = sg.exact_i8(34, 1, 255, m, n), sg.exact_i8(34, 2, 255, n, p)
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_s8(A, B)
+            tdt, odt = torch.int8, torch.int32
+        else:
+            A, B = sg.exact_f64(34, 1, 2049, m, n), sg.exact_f64(34, 2, 2049, n, p)
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_f64(A, B)
+            tdt, odt = torch.float64, torch.float64
+        big = torch.zeros(m + 7, p, dtype=odt, device="cuda")  # C_full inside a larger allocation
+        C_full = big[3:3 + m]
+        mm.gemm_sharded(m, n, p, tdt, tA, tB, None, layout=mm.MM_ROW_BLOCK, flags=mm.MM_GATHER_C_FUSED, root=0,
+                        C_full=C_full)
+        mm.sync_check()
+        assert np.array_equal(C_full.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
+        assert not big[:3].any() and not big[3 + m:].any()
+
+
 @pytest.mark.parametrize("panel", ["64", "2048"])
 def test_summa_world1_fp64(pg, panel):
     import paper_2408_15384_b200 as mm
