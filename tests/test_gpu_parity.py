@@ -246,6 +246,37 @@ def test_misaligned_operands_use_pack_path(mm, dt):
     check(dt, C.cpu().numpy(), Cref, D, exact=True)
 
 
+@pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
+def test_no_writes_outside_c(mm, dt):
+    """Bounds check of every store path (compute-sanitizer is closed on this pool): C lives
+    inside a larger buffer filled with a sentinel; the product must leave the guard bands,
+    and the row tails beyond p inside a wider pitch, untouched."""
+    out = {"f64": torch.float64, "bf16": torch.float32, "i8": torch.int32}[dt]
+    sentinel = -7
+    for (m, n, p, cg, nt) in [(300, 200, 520, 1, 1), (300, 200, 520, 2, 1), (513, 1024, 1100, 2, 2),
+                              (129, 64, 33, None, None), (1000, 2000, 260, None, None)]:
+        if dt == "f64" and cg == 2:
+            continue
+        A, B = gen(dt, "exact", 51, m, n, p, 255 if dt == "i8" else 9)
+        Cref, _ = ref(dt, A, B)
+        guard = 4096
+        buf = torch.full((guard + m * p + guard,), sentinel, dtype=out, device="cuda")
+        C = buf[guard:guard + m * p].view(m, p)
+        if cg:
+            os.environ["MM_FORCE_CG"] = str(cg)
+        if nt:
+            os.environ["MM_NT"] = str(nt)
+        try:
+            mm.gemm(to_dev(A, dt), to_dev(B, dt), out=C)
+            mm.sync_check()
+        finally:
+            os.environ.pop("MM_FORCE_CG", None)
+            os.environ.pop("MM_NT", None)
+        h = buf.cpu().numpy()
+        assert np.all(h[:guard] == sentinel) and np.all(h[guard + m * p:] == sentinel), (m, n, p, cg, nt)
+        assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64))
+
+
 def test_determinism(mm):
     for dt in ("bf16", "f64", "i8"):
         A, B = gen(dt, "random", 12, 700, 900, 650)
