@@ -260,6 +260,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-protocol", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -362,6 +363,42 @@ def main():
            "d2h_bytes_per_step": int(rows * P * 4 * world),
            "ms_per_step": e2e_s * 1e3, "api": "mm_gemm_host (pinned host A, B, C; synchronous call)"}
 
+    # ---- the paper's statistical protocol on per-launch times, rank-local
+    protocol = None
+    if rank == 0 and rows > 0 and not args.no_protocol:
+        from paper_2408_15384_b200 import protocol as pr
+
+        def launch_times(fn, k):
+            ts = []
+            for _ in range(k):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return ts
+        pilot = launch_times(step, 30)  # "30 preliminary tests"
+        reps = min(pr.repetitions_from_pilot(pilot), 400)
+        summ = pr.summarize(launch_times(step, reps))
+        sizes, tms = [], []
+        for nsz in (4096, 8192, 16384):
+            As, Bs = A[:nsz, :nsz].contiguous(), B[:nsz, :nsz].contiguous()
+            Cs = torch.empty(nsz, nsz, dtype=torch.float32, device="cuda")
+            sizes.append(nsz)
+            tms.append(pr.summarize(launch_times(lambda: mm.gemm(As, Bs, out=Cs), 15)).mean)
+        slope, r2 = pr.fit_complexity(sizes, tms)
+        mm.sync_check()
+        protocol = {
+            "pilot_runs": 30, "pilot_cv_pct": round(100 * pr.summarize(pilot).std_dev / pr.summarize(pilot).mean, 4),
+            "repetitions": reps, "rule": "n = 2((Z_0.975 + Z_0.8)/0.5)^2 s^2, s^2 in percent-of-mean units, min 15",
+            "mean_ms": round(summ.mean, 4), "ci95_half_width_ms": round(summ.ci95_half_width, 4),
+            "min_ms": round(summ.min, 4), "max_ms": round(summ.max, 4),
+            "tflops_at_mean": round(2.0 * rows * N_ * P / (summ.mean * 1e-3) / 1e12, 1),
+            "complexity": {"sizes": sizes, "mean_ms": [round(t, 4) for t in tms], "loglog_slope": round(slope, 3),
+                           "r2": round(r2, 5), "expected": "3 (PAPER.md:355)"},
+        }
+
     per_config = None
     if rank == 0 and not args.no_per_config:
         per_config = per_config_table(mm, peaks)
@@ -384,7 +421,7 @@ def main():
                        "parallelism": f"row-block x{world} (B resident on every rank)" if world > 1 else "single GPU",
                        "l2": "operands larger than L2 (A+B 1 GiB, C 1 GiB vs 126 MB): no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "with_comm": with_comm, "per_config": per_config,
+            "clocks": clocks, "with_comm": with_comm, "per_config": per_config, "protocol": protocol,
             "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
                                        "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
                                        "vs_spec_2250": round(value / world / 2250.0, 4)},

@@ -19,7 +19,7 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
   cat $OUT/bench_$TAG.json
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
-  CMD="python bench.py --steps 10 --warmup 3 --no-per-config --no-cpu-baseline"
+  CMD="python bench.py --steps 10 --warmup 3 --no-per-config --no-cpu-baseline --no-protocol"
   timeout 600 $CMD > $OUT/ncu_plain_$TAG.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
       --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1 && \
