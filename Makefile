@@ -38,3 +38,8 @@ $(MM_LIB): $(MM_SRCS) $(MM_HDRS)
 
 clean:
 	rm -f $(SG_LIB) $(OR_LIB) $(MM_LIB)
+
+SGC_LIB := synthgen/libsynthgen_cuda.so
+all: $(SGC_LIB)
+$(SGC_LIB): synthgen/synthgen_cuda.cu
+	$(NVCC) -std=c++17 -O3 $(GENCODE) -fmad=false -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -o $@ $<

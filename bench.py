@@ -17,9 +17,9 @@ Operands (1 GiB of A+B, 1 GiB of C) exceed the 126 MB L2, so no flush is needed
 between steps.  `e2e` = the same metric through mm_gemm_host with pinned host
 buffers (H2D of A, B and D2H of C inside the timed region).
 
-The other BASELINE.json configs are timed briefly into `per_config` (device
-inputs drawn with torch's seeded RNG in the same distributions; timing does not
-depend on values) next to cuBLAS on the same shapes.  Parity for every config
+The other BASELINE.json configs are timed briefly into `per_config` (inputs made
+on the GPU by synthgen/gpu.py from each config's seed, bit-identical to the host
+generator) next to cuBLAS on the same shapes.  Parity for every config
 lives in tests/ (pytest -m gpu), not here.
 
 --impl reference: the CPU oracle (oracle/, the paper's triple loop with the
@@ -175,28 +175,27 @@ def per_launch_ms(fn, reps, flush_buf=None):
 def per_config_table(mm, peaks):
     """Brief timings of the other BASELINE.json configs at N=1 (ours vs cuBLAS)."""
     import torch
-    g = torch.Generator(device="cuda")
+    from synthgen import gpu as sgg  # the synthgen recipe evaluated on the GPU (bit-identical)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     out = {}
     bf16_peak = peaks["bf16_tflops"]
     cases = [
-        ("configs[0] FP64 256^3 seed 0", "f64", 256, 256, 256, 30),
-        ("configs[1] FP64 2000x1500x1750 seed 1", "f64", 2000, 1500, 1750, 15),
-        ("configs[2] INT8 4096^3 seed 2", "i8", 4096, 4096, 4096, 15),
-        ("configs[4] FP64 32768^3 seed 4 (1 GPU)", "f64", 32768, 32768, 32768, 2),
+        ("configs[0] FP64 256^3 seed 0", "f64", 256, 256, 256, 0, 30),
+        ("configs[1] FP64 2000x1500x1750 seed 1", "f64", 2000, 1500, 1750, 1, 15),
+        ("configs[2] INT8 4096^3 seed 2", "i8", 4096, 4096, 4096, 2, 15),
+        ("configs[4] FP64 32768^3 seed 4 (1 GPU)", "f64", 32768, 32768, 32768, 4, 2),
     ]
-    for name, dt, m, n, p, reps in cases:
-        g.manual_seed(hash(name) & 0xFFFF)
+    for name, dt, m, n, p, seed, reps in cases:
         try:
             if dt == "f64":
-                A = torch.rand(m, n, device="cuda", dtype=torch.float64, generator=g).mul_(2).sub_(1)
-                B = torch.rand(n, p, device="cuda", dtype=torch.float64, generator=g).mul_(2).sub_(1)
+                A = sgg.uniform_f64(seed, 1, m, n)
+                B = sgg.uniform_f64(seed, 2, n, p)
                 ref = lambda: torch.matmul(A, B)  # noqa: E731
                 nominal = 37.0  # HGX-B200 FP64 / FP64-tensor dense, no measured FP64 peak in MEASURED_PEAKS.json
                 peak_note = "nominal FP64 37 TFLOP/s (HGX B200 spec)"
             else:
-                A = torch.randint(-127, 128, (m, n), device="cuda", dtype=torch.int8, generator=g)
-                B = torch.randint(-127, 128, (n, p), device="cuda", dtype=torch.int8, generator=g)
+                A = sgg.uniform_i8(seed, 1, m, n)
+                B = sgg.uniform_i8(seed, 2, n, p)
                 ref = lambda: torch._int_mm(A, B)  # noqa: E731
                 nominal = 2.0 * bf16_peak  # measured bf16 x nominal int8/bf16 ratio (4.5/2.25)
                 peak_note = "measured bf16 burst x 2 (nominal INT8:BF16 ratio)"
@@ -283,11 +282,16 @@ def main():
 
     # ---- inputs (synthgen recipe); each rank holds its row block of A and all of B
     r0, rows = mm.shard_range(M, world, rank)
-    A_full = sg.normal_bf16(SEED, sg.ROLE_A, M, N_)
-    B_host = sg.normal_bf16(SEED, sg.ROLE_B, N_, P)
-    A_host = np.ascontiguousarray(A_full[r0:r0 + rows])
-    A = torch.from_numpy(A_host.view(np.int16)).view(torch.bfloat16).cuda()
-    B = torch.from_numpy(B_host.view(np.int16)).view(torch.bfloat16).cuda()
+    # generated in HBM by the GPU evaluation of the synthgen recipe (bit-identical to the
+    # host generator, tests/test_synthgen_gpu.py); host copies serve e2e and cpu_baseline
+    from synthgen import gpu as sgg
+    A_dev_full = sgg.normal_bf16(SEED, sg.ROLE_A, M, N_)
+    B = sgg.normal_bf16(SEED, sg.ROLE_B, N_, P)
+    A = A_dev_full[r0:r0 + rows].contiguous()
+    del A_dev_full
+    A_host = A.view(torch.int16).cpu().numpy().view(np.uint16)
+    B_host = B.view(torch.int16).cpu().numpy().view(np.uint16)
+    A_full = A_host  # the cpu_baseline runs at N=1 only, where A_host is all of A
     C = torch.empty(rows, P, dtype=torch.float32, device="cuda")
     flops_total = 2.0 * M * N_ * P
 
