@@ -75,6 +75,7 @@ struct WorkSched {
   int nc;    // clusters
   int W;     // full data-parallel waves
   int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
+  int land;  // tail tiles split in exact halves: the finisher lands the partner's slab in its idle stage ring
   int64_t TI;  // tail iterations = tail tiles * num_kb
 
   __device__ __forceinline__ void tile_coords(int t, int& tm, int& tn) const {
@@ -138,13 +139,13 @@ __device__ __forceinline__ void store_row32(uint32_t* __restrict__ C, int64_t ld
   }
 }
 
-// Partial slabs are stored "row-interleaved": uint4 element (chunk c, vector i, row r) at
-// (c*8 + i)*128 + r, so a warp's 32 rows form one contiguous 512-B request (coalesced).
+// Partial slabs are stored warp-chunk-contiguous: uint4 element (chunk c, warp q, vector i,
+// lane l) at ((c*4 + q)*8 + i)*32 + l, so a warp's 32 rows x 32 columns of one chunk are
+// 4 KB in one piece (one bulk copy) and each vector i is one coalesced 512-B request.
+__device__ __forceinline__ size_t slab_index(int c, int q, int i, int l) { return ((size_t)(c * 4 + q) * 8 + i) * 32 + l; }
+
 template <bool I8>
-__device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict__ src /* = slab + c*8*128 + row */) {
-  uint4 w[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 128);  // 8 independent loads in flight
+__device__ __forceinline__ void add_words(uint32_t (&v)[32], const uint4 (&w)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t x[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
@@ -154,6 +155,14 @@ __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict
       else v[4 * i + u] = __float_as_uint(__uint_as_float(v[4 * i + u]) + __uint_as_float(x[u]));
     }
   }
+}
+
+template <bool I8>
+__device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict__ src /* = slab + slab_index(c,q,0,l) */) {
+  uint4 w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 32);  // 8 independent loads in flight
+  add_words<I8>(v, w);
 }
 
 template <bool I8, int CG, int NT>
@@ -175,7 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto empty_bar = [&](int s) { return bar0 + 8u * (Cfg::STAGES + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 4));
+  auto land_bar = [&](int q) { return bar0 + 8u * (2 * Cfg::STAGES + 4 + q); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 8));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -196,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 4 * CG);
     }
+    for (int qq = 0; qq < 4; ++qq) mbar_init(land_bar(qq), 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), 512);
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else if (kb0 != 0) {
         // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
-        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * Cfg::TILE_N)) + prow;
+        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * Cfg::TILE_N));
 #pragma unroll 1
         for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
           uint32_t v[32];
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            __stcg(slot + (c * 8 + i) * 128, make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+            __stcg(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
         }
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -384,14 +395,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             *(volatile unsigned*)(args.flags + (size_t)t * CG + rank) = 0u;  // reset for the next launch
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (sched.land && c_last == tail_c + 1) {
+          // Exact-halves split: this is the cluster's last item, so its operand ring is idle
+          // (all loads consumed, all MMAs retired).  Land the partner's slab there with one
+          // 4-KB bulk copy per chunk (all in flight at once), then add it from shared memory.
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(part + ((size_t)c_last * CG + rank) * (128 * Cfg::TILE_N));
+          if (lane == 0) {
+            mbar_arrive_expect_tx(land_bar((int)q), (Cfg::TILE_N / 32) * 4096u);
+            for (int c = 0; c < Cfg::TILE_N / 32; ++c)
+              bulk_copy_g2s(sA + (uint32_t)(c * 4 + q) * 4096u, src + slab_index(c, (int)q, 0, 0) * 16, 4096u,
+                            land_bar((int)q));
+          }
+          mbar_wait(land_bar((int)q), 0u, err, 7);
 #pragma unroll 1
-        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c * 32, v);
-          tmem_ld_wait();
-          for (int qq = tail_c + 1; qq <= c_last; ++qq)
-            add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * Cfg::TILE_N)) + c * 8 * 128 + prow);
-          emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+          for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, v);
+            uint4 w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              w[i] = *reinterpret_cast<const uint4*>(smem + (size_t)(c * 4 + q) * 4096 + i * 512 + lane * 16);
+            tmem_ld_wait();
+            add_words<I8>(v, w);
+            emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + c * 32, v);
+            tmem_ld_wait();
+            for (int qq = tail_c + 1; qq <= c_last; ++qq)
+              add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * Cfg::TILE_N)) +
+                               slab_index(c, (int)q, 0, (int)lane));
+            emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+          }
         }
       }
       tc_fence_before();
@@ -440,13 +478,23 @@ WorkSched make_sched(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, i
   s.TI = tail * s.num_kb;
   // The split tail pays for its partial-slab round trip only when there are many full waves
   // (measured: C4 55 waves +0.6 %, C3 3 waves -12 %; tools/ab_gpu.py).
-  bool split = tail > 0 && s.W >= 8;
-  if (const char* e = getenv("MM_STREAMK")) split = tail > 0 && atoi(e) != 0;  // tuning knob
-  if (!split) {
+  // Default: split the tail tiles into exact halves when there are enough clusters
+  // (2*tail <= nc) and 256-wide tiles (a 128 x 256 slab fits the idle operand ring of the
+  // finisher, which then lands its partner's slab with bulk copies); MM_STREAMK=1 forces
+  // the general split (partials read from global memory), MM_STREAMK=0 disables both.
+  // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
+  // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
+  int mode = (!i8 && tail > 0 && nt == 1 && 2 * tail <= s.nc && s.num_kb >= 8) ? 2 : 0;
+  if (const char* e = getenv("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
+  s.land = 0;
+  if (mode == 0) {
     // no stream-K tail: the last partial wave runs whole tiles
     s.W = (int)((T + s.nc - 1) / s.nc);
     s.ntc = 0;
     s.TI = 0;
+  } else if (mode == 2 && nt == 1 && 2 * tail <= s.nc) {
+    s.ntc = (int)(2 * tail);  // exact halves: finisher + one contributor per tile
+    s.land = 1;
   } else {
     // >= 4 k-blocks per segment, <= 4 segments per tile
     int64_t ntc = std::min<int64_t>(s.nc, tail * 4);
