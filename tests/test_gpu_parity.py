@@ -159,18 +159,26 @@ def test_tile_seams_f64(mm):
 
 @pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
 @pytest.mark.parametrize("cg", [1, 2])
-def test_stream_k_split_tiles(mm, dt, cg):
-    """Few tiles, long K: every tile is split over several CTAs/clusters (stream-K
-    partials + finisher), and a ragged split tail after full waves."""
-    if dt == "f64" and cg == 2:
-        pytest.skip("FP64 has no CTA-pair variant")
-    for (m, n, p) in [(512, 4096, 512), (130, 3000, 260), (2048, 2048, 2304), (1300, 1024, 2600)]:
-        A, B = gen(dt, "exact", 41, m, n, p, {"i8": 255, "bf16": 9, "f64": 2049}[dt])
-        Cref, D = ref(dt, A, B)
-        check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=True)
-        A, B = gen(dt, "random", 42, m, n, p)
-        Cref, D = ref(dt, A, B)
-        check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=False)
+@pytest.mark.parametrize("streamk", ["default", "1", "2"])
+def test_stream_k_split_tiles(mm, dt, cg, streamk):
+    """Few tiles, long K: tiles split over several CTAs/clusters (stream-K partials +
+    finisher) — default policy, the general split (1) and the exact-halves split with
+    landing in the operand ring (2) — and a ragged split tail after full waves."""
+    if dt == "f64" and (cg == 2 or streamk != "default"):
+        pytest.skip("FP64: no CTA pair; its stream-K is always on")
+    if streamk != "default":
+        os.environ["MM_STREAMK"] = streamk
+    try:
+        for (m, n, p) in [(512, 4096, 512), (130, 3000, 260), (2048, 2048, 2304), (1300, 1024, 2600),
+                          (2304, 1024, 2048)]:
+            A, B = gen(dt, "exact", 41, m, n, p, {"i8": 255, "bf16": 9, "f64": 2049}[dt])
+            Cref, D = ref(dt, A, B)
+            check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=True)
+            A, B = gen(dt, "random", 42, m, n, p)
+            Cref, D = ref(dt, A, B)
+            check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=False)
+    finally:
+        os.environ.pop("MM_STREAMK", None)
 
 
 @pytest.mark.parametrize("dt", ["i8", "bf16"])
