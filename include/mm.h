@@ -116,13 +116,20 @@ const char* mm_last_error(const mm_ctx* ctx);
  *   column block j of p) and of C (row block i of m, column block j of p),
  *   blocks by mm_shard_range on each axis.  k-panels of A are broadcast along
  *   grid rows and of B along grid columns; local products accumulate.
+ * MM_SUMMA_25D: 2.5D: G = grid_rows·grid_cols·c ranks form c
+ *   layers of that grid, rank r ↔ (l, i, j) with r = l·grid_rows·grid_cols +
+ *   i·grid_cols + j.  Every layer holds the same blocks (flag MM_REPLICATE:
+ *   only layer 0's are valid and are broadcast along the depth first); layer l
+ *   runs the SUMMA k-panels t ≡ l (mod c), and the layers' C blocks are summed
+ *   onto layer 0 (NCCL reduce); other layers' C_local hold partial sums.
+ *   SUMMA layouts are implemented for MM_F64 (they accumulate with β = 1).
  *
  * nccl_comm is an ncclComm_t spanning exactly the G ranks (e.g. torch's
  * ProcessGroupNCCL._comm_ptr()).  The library resolves NCCL symbols at run
  * time from the libnccl.so.2 already loaded in the process.
  */
-typedef enum { MM_ROW_BLOCK = 0, MM_SUMMA_2D = 1 } mm_layout;
-enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u, MM_GATHER_C_FUSED = 4u };
+typedef enum { MM_ROW_BLOCK = 0, MM_SUMMA_2D = 1, MM_SUMMA_25D = 2 } mm_layout;
+enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u, MM_GATHER_C_FUSED = 4u, MM_REPLICATE = 8u };
 
 mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                           mm_layout layout, int grid_rows, int grid_cols,

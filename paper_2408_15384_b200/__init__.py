@@ -18,12 +18,12 @@ import threading
 import torch
 
 from . import _lib
-from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_ROW_BLOCK, MM_S8_S32,
-                   MM_SUMMA_2D)
+from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE, MM_ROW_BLOCK,
+                   MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
 
 __all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "MMError", "Context",
            "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
-           "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED"]
+           "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D"]
 
 IN_DTYPE = {torch.float64: MM_F64, torch.bfloat16: MM_BF16_F32, torch.int8: MM_S8_S32}
 OUT_DTYPE = {MM_F64: torch.float64, MM_BF16_F32: torch.float32, MM_S8_S32: torch.int32}

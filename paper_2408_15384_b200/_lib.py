@@ -11,8 +11,8 @@ LIB_PATH = os.environ.get("MM_B200_LIB") or os.path.join(_HERE, "libmm_b200.so")
 
 MM_F64, MM_BF16_F32, MM_S8_S32 = 0, 1, 2
 MM_OK, MM_ERR_RUNTIME, MM_ERR_USAGE, MM_ERR_UNSUPPORTED, MM_ERR_WORKSPACE = 0, 1, 2, 3, 4
-MM_ROW_BLOCK, MM_SUMMA_2D = 0, 1
-MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED = 1, 2, 4
+MM_ROW_BLOCK, MM_SUMMA_2D, MM_SUMMA_25D = 0, 1, 2
+MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE = 1, 2, 4, 8
 
 # every symbol include/mm.h declares
 EXPORTS = (

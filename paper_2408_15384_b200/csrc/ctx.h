@@ -31,6 +31,8 @@ struct mm_ctx {
   size_t sbuf_bytes[4] = {0, 0, 0, 0};
   void* row_comm = nullptr;  // SUMMA sub-communicators (ncclComm_t), cached per parent/grid
   void* col_comm = nullptr;
+  void* depth_comm = nullptr;  // 2.5D layer communicator
+  int split_layers = 0;
   void* split_parent = nullptr;
   int split_rows = 0, split_cols = 0;
   void* sk_ws = nullptr;  // stream-K partial tiles (both kernels)

@@ -42,6 +42,8 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t) =
+      nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
@@ -67,6 +69,7 @@ const NcclApi& nccl() {
     LOAD(Send, "ncclSend");
     LOAD(Recv, "ncclRecv");
     LOAD(AllReduce, "ncclAllReduce");
+    LOAD(Reduce, "ncclReduce");
     LOAD(GroupStart, "ncclGroupStart");
     LOAD(GroupEnd, "ncclGroupEnd");
     LOAD(CommSplit, "ncclCommSplit");
@@ -75,7 +78,7 @@ const NcclApi& nccl() {
     LOAD(CommUserRank, "ncclCommUserRank");
     LOAD(GetErrorString, "ncclGetErrorString");
 #undef LOAD
-    g_nccl.ok = g_nccl.Broadcast && g_nccl.AllReduce && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
+    g_nccl.ok = g_nccl.Broadcast && g_nccl.AllReduce && g_nccl.Reduce && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
                 g_nccl.CommSplit && g_nccl.CommCount && g_nccl.CommUserRank && g_nccl.GetErrorString;
   });
   return g_nccl;
@@ -227,8 +230,9 @@ void mm_release_comms(mm_ctx* ctx) {
   if (api.CommDestroy) {
     if (ctx->row_comm) api.CommDestroy(static_cast<ncclComm_t>(ctx->row_comm));
     if (ctx->col_comm) api.CommDestroy(static_cast<ncclComm_t>(ctx->col_comm));
+    if (ctx->depth_comm) api.CommDestroy(static_cast<ncclComm_t>(ctx->depth_comm));
   }
-  ctx->row_comm = ctx->col_comm = nullptr;
+  ctx->row_comm = ctx->col_comm = ctx->depth_comm = nullptr;
   ctx->split_parent = nullptr;
 }
 
@@ -284,31 +288,54 @@ static mm_status row_block(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtyp
   return MM_OK;
 }
 
+// SUMMA over a pr × pc grid, replicated over `layers` depth layers (2.5D, Solomonik &
+// Demmel; "2.5D Matrix Multiplication").  Rank r ↔ (layer l, gi, gj) with
+// r = l·pr·pc + gi·pc + gj.  Every layer holds the same A/B blocks; layer l runs the SUMMA
+// k-panels t ≡ l (mod layers), so each layer broadcasts 1/layers of the panels, and the
+// layers' partial C blocks are summed onto layer 0 by an NCCL reduce along the depth
+// communicator.  layers = 1 is plain SUMMA.
 static mm_status summa_2d(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, int pr, int pc,
-                          const void* A_local, const void* B_local, void* C_local, ncclComm_t comm, int r,
-                          cudaStream_t s) {
+                          int layers, const void* A_local, const void* B_local, void* C_local, ncclComm_t comm,
+                          int r, unsigned flags, cudaStream_t s) {
   const NcclApi& api = nccl();
   if (dtype != MM_F64)
-    return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_SUMMA_2D accumulates across k-panels; implemented for MM_F64");
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_SUMMA_2D/25D accumulate across k-panels; implemented for MM_F64");
   const size_t ei = dtype_in_size(dtype);
-  const int gi = r / pc, gj = r % pc;
-  // sub-communicators: grid row (color gi, rank gj) and grid column (color gj, rank gi)
-  if (ctx->split_parent != comm || ctx->split_rows != pr || ctx->split_cols != pc) {
+  const int l = r / (pr * pc), r2 = r % (pr * pc);
+  const int gi = r2 / pc, gj = r2 % pc;
+  // sub-communicators: grid row (color l·pr+gi, rank gj), grid column (color l·pc+gj, rank gi),
+  // depth (color gi·pc+gj, rank l)
+  if (ctx->split_parent != comm || ctx->split_rows != pr || ctx->split_cols != pc || ctx->split_layers != layers) {
     mm_release_comms(ctx);
-    ncclComm_t rc = nullptr, cc = nullptr;
-    NCCL_CHECK(ctx, api.CommSplit(comm, gi, gj, &rc, nullptr));
-    NCCL_CHECK(ctx, api.CommSplit(comm, gj, gi, &cc, nullptr));
+    ncclComm_t rc = nullptr, cc = nullptr, dc = nullptr;
+    NCCL_CHECK(ctx, api.CommSplit(comm, l * pr + gi, gj, &rc, nullptr));
+    NCCL_CHECK(ctx, api.CommSplit(comm, l * pc + gj, gi, &cc, nullptr));
+    if (layers > 1) NCCL_CHECK(ctx, api.CommSplit(comm, gi * pc + gj, l, &dc, nullptr));
     ctx->row_comm = rc;
     ctx->col_comm = cc;
+    ctx->depth_comm = dc;
     ctx->split_parent = comm;
     ctx->split_rows = pr;
     ctx->split_cols = pc;
+    ctx->split_layers = layers;
   }
   ncclComm_t row_comm = static_cast<ncclComm_t>(ctx->row_comm);
   ncclComm_t col_comm = static_cast<ncclComm_t>(ctx->col_comm);
+  ncclComm_t depth_comm = static_cast<ncclComm_t>(ctx->depth_comm);
 
   const Range am = shard(m, pr, gi), ak = shard(n, pc, gj);  // my A block: rows am, cols ak
   const Range bk = shard(n, pr, gi), bn = shard(p, pc, gj);  // my B block: rows bk, cols bn
+  if (layers > 1 && (flags & MM_REPLICATE)) {
+    // the caller placed the blocks on layer 0 only: replicate them along the depth
+    NCCL_CHECK(ctx, api.GroupStart());
+    if (am.count > 0 && ak.count > 0)
+      NCCL_CHECK(ctx, api.Broadcast(A_local, const_cast<void*>(A_local), (size_t)(am.count * ak.count) * ei, ncclUint8,
+                                    0, depth_comm, s));
+    if (bk.count > 0 && bn.count > 0)
+      NCCL_CHECK(ctx, api.Broadcast(B_local, const_cast<void*>(B_local), (size_t)(bk.count * bn.count) * ei, ncclUint8,
+                                    0, depth_comm, s));
+    NCCL_CHECK(ctx, api.GroupEnd());
+  }
   int64_t panel = 2048;
   if (const char* e = getenv("MM_SUMMA_PANEL")) panel = std::max<int64_t>(16, atoll(e));
   const int np = mm_summa_panels(n, pr, pc, panel, 0, nullptr, nullptr, nullptr, nullptr);
@@ -337,11 +364,12 @@ static mm_status summa_2d(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
   cudaStreamWaitEvent(sc, ev_start, 0);
   // C block starts at zero if some panel never reaches us (empty k range cannot happen: n >= 1)
   st = MM_OK;
-  for (int t = 0; t < np && st == MM_OK; ++t) {
-    const int b = t & 1;
+  int done = 0;  // panels this layer has accumulated
+  for (int t = l; t < np && st == MM_OK; t += layers) {
+    const int b = (t / layers) & 1;
     uint8_t* Ap = static_cast<uint8_t*>(ctx->sbuf[2 * b]);
     uint8_t* Bp = static_cast<uint8_t*>(ctx->sbuf[2 * b + 1]);
-    if (t >= 2) cudaStreamWaitEvent(sc, ev_free[b], 0);
+    if (done >= 2) cudaStreamWaitEvent(sc, ev_free[b], 0);
     // owners stage their panel into the send buffer (A: a column slice → pitched copy; B: whole rows)
     if (gj == ao[t] && am.count > 0) {
       const uint8_t* src = static_cast<const uint8_t*>(A_local) + (size_t)(k0[t] - ak.start) * ei;
@@ -372,8 +400,10 @@ static mm_status summa_2d(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
     cudaEventRecord(ev_ready[b], sc);
     cudaStreamWaitEvent(s, ev_ready[b], 0);
     if (am.count > 0 && bn.count > 0)
-      st = gemm_ld(ctx, am.count, kw[t], bn.count, dtype, Ap, kw[t], Bp, bn.count, C_local, bn.count, t > 0 ? 1 : 0, s);
+      st = gemm_ld(ctx, am.count, kw[t], bn.count, dtype, Ap, kw[t], Bp, bn.count, C_local, bn.count, done > 0 ? 1 : 0,
+                   s);
     cudaEventRecord(ev_free[b], s);
+    ++done;
   }
   // the caller's stream must not run ahead of the last communication
   cudaEvent_t ev_end;
@@ -386,7 +416,14 @@ static mm_status summa_2d(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
     cudaEventDestroy(ev_free[b]);
   }
   cudaEventDestroy(ev_start);
-  return st;
+  if (st != MM_OK) return st;
+  if (layers > 1 && am.count > 0 && bn.count > 0) {
+    // a layer that received no panel contributes zeros; then sum the layers onto layer 0
+    if (done == 0 && cudaMemsetAsync(C_local, 0, (size_t)(am.count * bn.count) * ei, s) != cudaSuccess)
+      return set_err(ctx, MM_ERR_RUNTIME, "zeroing C_local failed");
+    NCCL_CHECK(ctx, api.Reduce(C_local, C_local, (size_t)(am.count * bn.count), ncclFloat64, ncclSum, 0, depth_comm, s));
+  }
+  return MM_OK;
 }
 
 __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
@@ -419,7 +456,14 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
     if (grid_rows < 1 || grid_cols < 1 || grid_rows * grid_cols != G)
       return set_err(ctx, MM_ERR_USAGE, "grid %d x %d does not match communicator size %d", grid_rows, grid_cols, G);
     if (flags) return set_err(ctx, MM_ERR_USAGE, "MM_SUMMA_2D takes no flags (operands and C stay block-distributed)");
-    return summa_2d(ctx, m, n, p, dtype, grid_rows, grid_cols, A_local, B_local, C_local, comm, r, s);
+    return summa_2d(ctx, m, n, p, dtype, grid_rows, grid_cols, 1, A_local, B_local, C_local, comm, r, 0, s);
+  }
+  if (layout == MM_SUMMA_25D) {
+    if (grid_rows < 1 || grid_cols < 1 || G % (grid_rows * grid_cols) != 0)
+      return set_err(ctx, MM_ERR_USAGE, "grid %d x %d does not divide communicator size %d", grid_rows, grid_cols, G);
+    if (flags & ~(unsigned)MM_REPLICATE) return set_err(ctx, MM_ERR_USAGE, "MM_SUMMA_25D takes only MM_REPLICATE");
+    return summa_2d(ctx, m, n, p, dtype, grid_rows, grid_cols, G / (grid_rows * grid_cols), A_local, B_local, C_local,
+                    comm, r, flags, s);
   }
   return set_err(ctx, MM_ERR_USAGE, "unknown layout %d", (int)layout);
 }

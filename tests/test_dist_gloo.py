@@ -93,6 +93,52 @@ def _summa_worker(rank, world, port, m, n, p, pr, pc, panel, q):
         dist.destroy_process_group()
 
 
+def _summa25_worker(rank, world, port, m, n, p, pr, pc, panel, q):
+    """MM_SUMMA_25D schedule: layer l = rank // (pr*pc) runs the SUMMA panels t ≡ l (mod c)
+    on its copy of the blocks (MM_REPLICATE: broadcast from layer 0 along the depth), then
+    the layers' C blocks are summed onto layer 0."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = world // (pr * pc)
+        A, B = _inputs(m, n, p)
+        l, r2 = rank // (pr * pc), rank % (pr * pc)
+        gi, gj = r2 // pc, r2 % pc
+        am, ak = mm.shard_range(m, pr, gi), mm.shard_range(n, pc, gj)
+        bk, bn = mm.shard_range(n, pr, gi), mm.shard_range(p, pc, gj)
+        rank_of = lambda ll, i, j: ll * pr * pc + i * pc + j  # noqa: E731
+        row_groups = {(ll, i): dist.new_group([rank_of(ll, i, j) for j in range(pc)]) for ll in range(c) for i in range(pr)}
+        col_groups = {(ll, j): dist.new_group([rank_of(ll, i, j) for i in range(pr)]) for ll in range(c) for j in range(pc)}
+        depth_groups = {(i, j): dist.new_group([rank_of(ll, i, j) for ll in range(c)]) for i in range(pr) for j in range(pc)}
+        # MM_REPLICATE: only layer 0 holds the blocks
+        A_loc = torch.zeros(am[1], ak[1], dtype=torch.float64)
+        B_loc = torch.zeros(bk[1], bn[1], dtype=torch.float64)
+        if l == 0:
+            A_loc[:] = torch.from_numpy(np.ascontiguousarray(A[am[0]:am[0] + am[1], ak[0]:ak[0] + ak[1]]))
+            B_loc[:] = torch.from_numpy(np.ascontiguousarray(B[bk[0]:bk[0] + bk[1], bn[0]:bn[0] + bn[1]]))
+        dist.broadcast(A_loc, src=rank_of(0, gi, gj), group=depth_groups[(gi, gj)])
+        dist.broadcast(B_loc, src=rank_of(0, gi, gj), group=depth_groups[(gi, gj)])
+        A_loc, B_loc = A_loc.numpy(), B_loc.numpy()
+        C_loc = torch.zeros(am[1], bn[1], dtype=torch.float64)
+        panels = mm.summa_panels(n, pr, pc, panel)
+        for t in range(l, len(panels), c):
+            k0, kw, ao, bo = panels[t]
+            Ap = torch.zeros(am[1], kw, dtype=torch.float64)
+            if gj == ao:
+                Ap[:] = torch.from_numpy(np.ascontiguousarray(A_loc[:, k0 - ak[0]:k0 - ak[0] + kw]))
+            dist.broadcast(Ap, src=rank_of(l, gi, ao), group=row_groups[(l, gi)])
+            Bp = torch.zeros(kw, bn[1], dtype=torch.float64)
+            if gi == bo:
+                Bp[:] = torch.from_numpy(np.ascontiguousarray(B_loc[k0 - bk[0]:k0 - bk[0] + kw]))
+            dist.broadcast(Bp, src=rank_of(l, bo, gj), group=col_groups[(l, gj)])
+            C_loc += torch.from_numpy(oracle.gemm_f64(Ap.numpy(), Bp.numpy()))
+        dist.reduce(C_loc, dst=rank_of(0, gi, gj), op=dist.ReduceOp.SUM, group=depth_groups[(gi, gj)])
+        if l == 0:
+            q.put(("blk", rank, C_loc.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
 def _spawn(target, args, world):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
@@ -129,4 +175,18 @@ def test_summa_world2_equals_single_process(pr, pc, m, n, p, panel):
         gi, gj = rank // pc, rank % pc
         am, bn = mm.shard_range(m, pr, gi), mm.shard_range(p, pc, gj)
         # exact-integer entries: every summation order gives the same bits
+        assert np.array_equal(blk, C[am[0]:am[0] + am[1], bn[0]:bn[0] + bn[1]])
+
+
+@pytest.mark.parametrize("world,pr,pc", [(2, 1, 1), (4, 2, 1), (4, 1, 2)])
+@pytest.mark.parametrize("m,n,p,panel", [(37, 41, 29, 8), (9, 3, 11, 1)])
+def test_summa25d_equals_single_process(world, pr, pc, m, n, p, panel):
+    out = _spawn(_summa25_worker, (m, n, p, pr, pc, panel), world)
+    A, B = _inputs(m, n, p)
+    C = oracle.gemm_f64(A, B)
+    blocks = {o[1]: o[2] for o in out if o[0] == "blk"}
+    assert len(blocks) == pr * pc  # layer 0 holds the result
+    for rank, blk in blocks.items():
+        gi, gj = rank // pc, rank % pc
+        am, bn = mm.shard_range(m, pr, gi), mm.shard_range(p, pc, gj)
         assert np.array_equal(blk, C[am[0]:am[0] + am[1], bn[0]:bn[0] + bn[1]])

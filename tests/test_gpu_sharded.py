@@ -124,3 +124,16 @@ def test_sharded_usage_errors(pg):
         mm.gemm_sharded(4, 4, 4, torch.float64, t, t.clone(), t.clone(), layout=mm.MM_SUMMA_2D, grid=(2, 1))
     with pytest.raises(mm.MMError, match="root"):
         mm.gemm_sharded(4, 4, 4, torch.float64, t, t.clone(), t.clone(), layout=mm.MM_ROW_BLOCK, root=3)
+
+
+def test_summa25d_world1_fp64(pg):
+    """MM_SUMMA_25D at world size 1 (one layer of a 1x1 grid): the layer/panel/reduce code
+    path with the real NCCL calls; the multi-layer schedule is checked over gloo."""
+    import paper_2408_15384_b200 as mm
+    m, n, p = 500, 3000, 700
+    A, B = sg.exact_f64(35, 1, 2049, m, n), sg.exact_f64(35, 2, 2049, n, p)
+    C = torch.empty(m, p, dtype=torch.float64, device="cuda")
+    mm.gemm_sharded(m, n, p, torch.float64, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), C,
+                    layout=mm.MM_SUMMA_25D, grid=(1, 1), flags=mm.MM_REPLICATE)
+    mm.sync_check()
+    assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
