@@ -242,28 +242,91 @@ static mm_status row_block(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtyp
   const NcclApi& api = nccl();
   const size_t ei = dtype_in_size(dtype), eo = dtype_out_size(dtype);
   const Range mine = shard(m, G, r);
-  if (flags & MM_BCAST_B)
-    NCCL_CHECK(ctx, api.Broadcast(B_local, B_local, (size_t)(n * p) * ei, ncclUint8, root, comm, s));
+
+  // Where this rank's C rows go: its own C_local, or (MM_GATHER_C_FUSED) straight into the
+  // root's C_full over NVLink — GEMM -> gather as ONE kernel per rank (TMA stores to peer memory).
+  uint8_t* target = static_cast<uint8_t*>(C_local);
   if (flags & MM_GATHER_C_FUSED) {
-    // GEMM -> gather as ONE kernel per rank: the epilogue's TMA stores target the root's
-    // C_full (peer memory over NVLink), rows [row0, row0+rows).
     if (r == root && !C_full) return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C_FUSED needs C_full on the root rank");
-    uint8_t* target = nullptr;
-    mm_status st = peer_pointer_of_root(ctx, C_full, root, r, comm, s, &target);
+    uint8_t* full = nullptr;
+    mm_status st = peer_pointer_of_root(ctx, C_full, root, r, comm, s, &full);
     if (st != MM_OK) return st;
-    if (mine.count > 0) {
-      st = gemm_ld(ctx, mine.count, n, p, dtype, A_local, n, B_local, p, target + mine.start * p * eo, p, 0, s);
-      if (st != MM_OK) return st;
+    target = full + mine.start * p * eo;
+  }
+
+  if (flags & MM_BCAST_B) {
+    // B broadcast in column panels, double-buffered on a communication stream, so the
+    // broadcast of panel j+1 overlaps the product C[:, panel j] = A · B[:, panel j].
+    int64_t npan = 8;
+    if (const char* e = getenv("MM_BCAST_PANELS")) npan = std::max<int64_t>(1, atoll(e));  // tuning knob
+    int64_t w = (p + npan - 1) / npan;
+    w = (w + 15) / 16 * 16;  // 16-element multiple: every panel pitch is 16-B aligned for TMA
+    if (w > p) w = p;
+    const int64_t J = (p + w - 1) / w;
+    mm_status st;
+    for (int b = 0; b < 2; ++b)
+      if ((st = ensure_buffer(ctx, &ctx->sbuf[b], &ctx->sbuf_bytes[b], (size_t)(n * w) * ei)) != MM_OK) return st;
+    if (!ctx->s_in && cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking) != cudaSuccess)
+      return set_err(ctx, MM_ERR_RUNTIME, "stream creation failed");
+    cudaStream_t sc = ctx->s_in;
+    cudaEvent_t ev_start, ev_ready[2], ev_free[2], ev_end;
+    cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventCreateWithFlags(&ev_ready[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming);
     }
-    // barrier: the root's C_full is complete once every rank's product kernel has finished
+    cudaEventRecord(ev_start, s);
+    cudaStreamWaitEvent(sc, ev_start, 0);
+    st = MM_OK;
+    for (int64_t j = 0; j < J && st == MM_OK; ++j) {
+      const int b = (int)(j & 1);
+      const int64_t c0 = j * w, wj = std::min(w, p - c0);
+      uint8_t* stage = static_cast<uint8_t*>(ctx->sbuf[b]);
+      uint8_t* Bcol = static_cast<uint8_t*>(B_local) + c0 * ei;
+      if (j >= 2) cudaStreamWaitEvent(sc, ev_free[b], 0);
+      if (r == root && cudaMemcpy2DAsync(stage, (size_t)wj * ei, Bcol, (size_t)p * ei, (size_t)wj * ei, (size_t)n,
+                                         cudaMemcpyDeviceToDevice, sc) != cudaSuccess) {
+        st = set_err(ctx, MM_ERR_RUNTIME, "B panel staging failed");
+        break;
+      }
+      ncclResult_t nr = api.Broadcast(stage, stage, (size_t)(n * wj) * ei, ncclUint8, root, comm, sc);
+      if (nr != ncclSuccess) {
+        st = set_err(ctx, MM_ERR_RUNTIME, "B panel broadcast failed: %s", api.GetErrorString(nr));
+        break;
+      }
+      // keep the contract "B_local holds B afterwards" on every rank (off the critical path)
+      if (r != root && cudaMemcpy2DAsync(Bcol, (size_t)p * ei, stage, (size_t)wj * ei, (size_t)wj * ei, (size_t)n,
+                                         cudaMemcpyDeviceToDevice, sc) != cudaSuccess) {
+        st = set_err(ctx, MM_ERR_RUNTIME, "B panel copy-out failed");
+        break;
+      }
+      cudaEventRecord(ev_ready[b], sc);
+      cudaStreamWaitEvent(s, ev_ready[b], 0);
+      if (mine.count > 0)
+        st = gemm_ld(ctx, mine.count, n, wj, dtype, A_local, n, stage, wj, target + c0 * eo, p, 0, s);
+      cudaEventRecord(ev_free[b], s);
+    }
+    cudaEventRecord(ev_end, sc);
+    cudaStreamWaitEvent(s, ev_end, 0);
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_end);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(ev_ready[b]);
+      cudaEventDestroy(ev_free[b]);
+    }
+    if (st != MM_OK) return st;
+  } else if (mine.count > 0) {
+    mm_status st = gemm_ld(ctx, mine.count, n, p, dtype, A_local, n, B_local, p, target, p, 0, s);
+    if (st != MM_OK) return st;
+  }
+
+  if (flags & MM_GATHER_C_FUSED) {
+    // barrier: the root's C_full is complete once every rank's product kernels have finished
     if (!ctx->bar_buf && cudaMalloc(&ctx->bar_buf, 16) != cudaSuccess)
       return set_err(ctx, MM_ERR_WORKSPACE, "barrier buffer allocation failed");
     NCCL_CHECK(ctx, api.AllReduce(ctx->bar_buf, ctx->bar_buf, 1, ncclInt32, ncclSum, comm, s));
     return MM_OK;
-  }
-  if (mine.count > 0) {
-    mm_status st = gemm_ld(ctx, mine.count, n, p, dtype, A_local, n, B_local, p, C_local, p, 0, s);
-    if (st != MM_OK) return st;
   }
   if (flags & MM_GATHER_C) {
     if (r == root && !C_full) return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C needs C_full on the root rank");

@@ -87,7 +87,8 @@ def test_row_block_fused_gather_world1(pg):
             tdt, odt = torch.float64, torch.float64
         big = torch.zeros(m + 7, p, dtype=odt, device="cuda")  # C_full inside a larger allocation
         C_full = big[3:3 + m]
-        mm.gemm_sharded(m, n, p, tdt, tA, tB, None, layout=mm.MM_ROW_BLOCK, flags=mm.MM_GATHER_C_FUSED, root=0,
+        flags = mm.MM_GATHER_C_FUSED | (mm.MM_BCAST_B if dt != "f64" else 0)  # + panel-chunked broadcast
+        mm.gemm_sharded(m, n, p, tdt, tA, tB, None, layout=mm.MM_ROW_BLOCK, flags=flags, root=0,
                         C_full=C_full)
         mm.sync_check()
         assert np.array_equal(C_full.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
