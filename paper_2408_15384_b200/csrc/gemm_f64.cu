@@ -118,7 +118,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wn = (int)warp & 3;   // 0..3 : cols wn*(BN/4)
     const int g = (int)lane >> 2;   // fragment row / column index 0..7
     const int kk = (int)lane & 3;   // fragment k index 0..3
-    const int kofs = (kk & 1) + ((kk >> 1) << 2);  // k within quad: {0,1,4,5}
+    // Conflict-free fragment loads (LDS.64 is served per half-warp: lanes 0-15 then 16-31).
+    // Each DMMA takes the four consecutive k's of its quad; the 8 A rows of a fragment are
+    // permuted so a half-warp's rows have (r & 7) ∈ {0,2,4,6} / {1,3,5,7}, and the 8 B
+    // columns are permuted to {0,1,8,9,2,3,10,11} (+4 for odd n-tiles) inside a 16-column
+    // box; the epilogue writes D back through the same permutations.
+    const int arow = (g < 4) ? 2 * g : 2 * (g - 4) + 1;           // A/D row of fragment row g
+    const int bcol = (g & 1) + (((g >> 1) & 1) << 3) + ((g >> 2) << 1);  // B column of fragment col g
+    const int dcol = ((kk & 1) << 3) + ((kk >> 1) << 1);          // first of this thread's 2 D columns
     double* C = reinterpret_cast<double*>(args.C);
     double* part = reinterpret_cast<double*>(args.ws);
     const bool vec_ok = ((args.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
@@ -144,16 +151,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES;
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const int k = ((qd & 1) << 1) + ((qd >> 1) << 3) + kofs;  // quad bases 0,2,8,10
+          const int k = qd * 4 + kk;
           double af[Cfg::MI], bf[Cfg::NI];
 #pragma unroll
           for (int mi = 0; mi < Cfg::MI; ++mi) {
-            const int r = wm * (BM / 2) + mi * 8 + g;
+            const int r = wm * (BM / 2) + mi * 8 + arow;
             af[mi] = *reinterpret_cast<const double*>(pa + r * 128 + (((k >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3));
           }
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int cc = wn * (BN / 4) + ni * 8 + g;
+            const int cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + bcol;
             const int c16 = cc & 15;
             bf[ni] = *reinterpret_cast<const double*>(pb + (cc >> 4) * BBOX_BYTES + k * 128 +
                                                       (((c16 >> 1) ^ (k & 7)) << 4) + ((c16 & 1) << 3));
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int r = wm * (BM / 2) + mi * 8 + g, cc = wn * (BN / 4) + ni * 8 + kk * 2;
+            const int r = wm * (BM / 2) + mi * 8 + arow, cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
             __stcg(reinterpret_cast<double2*>(slot + r * BN + cc), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
           }
         __threadfence();
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
               for (int ni = 0; ni < Cfg::NI; ++ni) {
-                const int r = wm * (BM / 2) + mi * 8 + g, cc = wn * (BN / 4) + ni * 8 + kk * 2;
+                const int r = wm * (BM / 2) + mi * 8 + arow, cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
                 const double2 v = __ldcg(reinterpret_cast<const double2*>(slot + r * BN + cc));
                 acc[mi][ni][0] += v.x;
                 acc[mi][ni][1] += v.y;
@@ -209,11 +216,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- epilogue: registers -> global (predicated on the ragged edges), β ∈ {0, 1}
 #pragma unroll
         for (int mi = 0; mi < Cfg::MI; ++mi) {
-          const int64_t row = (int64_t)tm * BM + wm * (BM / 2) + mi * 8 + g;
+          const int64_t row = (int64_t)tm * BM + wm * (BM / 2) + mi * 8 + arow;
           if (row >= args.M) continue;
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int64_t col = (int64_t)tn * BN + wn * (BN / 4) + ni * 8 + kk * 2;
+            const int64_t col = (int64_t)tn * BN + wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
             double* dst = C + row * args.ldc + col;
             double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
             if (vec_ok && col + 1 < args.N) {
