@@ -126,6 +126,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int arow = (g < 4) ? 2 * g : 2 * (g - 4) + 1;           // A/D row of fragment row g
     const int bcol = (g & 1) + (((g >> 1) & 1) << 3) + ((g >> 2) << 1);  // B column of fragment col g
     const int dcol = ((kk & 1) << 3) + ((kk >> 1) << 1);          // first of this thread's 2 D columns
+    // k = qd*4 + kk.  A: row r = wm*BM/2 + mi*8 + arow (r & 7 == arow), 16-B chunk k>>1, half k&1.
+    const int a_base0 = (wm * (BM / 2) + arow) * 128 + (kk & 1) * 8;
+    const int a_x0 = (kk >> 1) ^ arow;
+    // B: column c16 = (ni&1)*4 + bcol in box wn*BN/64 + ni/2; chunk (c16>>1) ^ (k & 7), half c16 & 1.
+    const int b_base0 = wn * (BN / 64) * BBOX_BYTES + kk * 128 + (bcol & 1) * 8;
+    const int b_x0 = (bcol >> 1) ^ kk;
     double* C = reinterpret_cast<double*>(args.C);
     double* part = reinterpret_cast<double*>(args.ws);
     const bool vec_ok = ((args.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
@@ -149,26 +155,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!mbar_wait(full_bar(stage), phase, err, 12)) { ok = false; break; }
         const uint8_t* pa = smem + stage * Cfg::A_BYTES;
         const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES;
+        int a_base, a_x, b_base, b_x;
+        asm volatile("mov.b32 %0, %1;" : "=r"(a_base) : "r"(a_base0));
+        asm volatile("mov.b32 %0, %1;" : "=r"(a_x) : "r"(a_x0));
+        asm volatile("mov.b32 %0, %1;" : "=r"(b_base) : "r"(b_base0));
+        asm volatile("mov.b32 %0, %1;" : "=r"(b_x) : "r"(b_x0));
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
           const int k = qd * 4 + kk;
-          double af[Cfg::MI], bf[Cfg::NI];
+          // Fragment addresses from two thread constants re-materialised per k-block (opaque
+          // to the compiler, so it does not hoist 16+ loop-invariant addresses and spill them):
+          //   A: pa + a_base + (((qd<<1) ^ a_x) << 4) + mi*1024
+          //   B: pb + b_base + (((ni&1)<<1 ^ (qd&1)<<2 ^ b_x) << 4) + (ni>>1)*BBOX + qd*512
+          double bf[Cfg::NI];
+#pragma unroll
+          for (int ni = 0; ni < Cfg::NI; ++ni)
+            bf[ni] = *reinterpret_cast<const double*>(
+                pb + b_base + ((((ni & 1) << 1) ^ ((qd & 1) << 2) ^ b_x) << 4) + (ni >> 1) * BBOX_BYTES + qd * 512);
+          const uint8_t* pa_q = pa + a_base + ((((qd << 1) & 7) ^ a_x) << 4) + ((qd << 1) & 8) * 16;
 #pragma unroll
           for (int mi = 0; mi < Cfg::MI; ++mi) {
-            const int r = wm * (BM / 2) + mi * 8 + arow;
-            af[mi] = *reinterpret_cast<const double*>(pa + r * 128 + (((k >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3));
+            const double af = *reinterpret_cast<const double*>(pa_q + mi * 1024);  // row + 8*mi keeps r & 7
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
           }
-#pragma unroll
-          for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + bcol;
-            const int c16 = cc & 15;
-            bf[ni] = *reinterpret_cast<const double*>(pb + (cc >> 4) * BBOX_BYTES + k * 128 +
-                                                      (((c16 >> 1) ^ (k & 7)) << 4) + ((c16 & 1) << 3));
-          }
-#pragma unroll
-          for (int mi = 0; mi < Cfg::MI; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < Cfg::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_bar(stage));
