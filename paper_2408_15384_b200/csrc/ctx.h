@@ -42,6 +42,7 @@ struct mm_ctx {
   void* ipc_xchg = nullptr;  // device staging for the IPC handle exchange (fused gather)
   std::vector<std::pair<std::string, void*>> ipc_open;  // opened peer allocations (handle bytes -> base)
   void* bar_buf = nullptr;   // one int for the communicator barrier
+  void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   uint64_t launches = 0;  // kernels launched by this context
   std::string last_error;
 };

@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // optional timeline (MM_TRACE=1): per CTA ns spent waiting, by role
+  uint64_t tr_barrier = 0, tr_empty = 0, tr_tempty = 0, tr_full = 0, tr_tfull = 0;
+  const uint64_t tr_t0 = args.trace ? globaltimer_ns() : 0;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -230,15 +233,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         // Wave barrier: start item j only when every CTA has issued all loads of its
         // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
+        const uint64_t tb0 = args.trace ? globaltimer_ns() : 0;
         if (args.wave_sync && j > 0 && j <= sched.W &&
             !counter_wait(args.sync, (unsigned)j * gridDim.x, err, 5))
           break;
+        if (args.trace) tr_barrier += globaltimer_ns() - tb0;
         int tm, tn;
         sched.tile_coords(t, tm, tn);
         const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = tn * Cfg::TILE_N + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
         for (int kb = kb0; kb < kb1; ++kb) {
+          const uint64_t te0 = args.trace ? globaltimer_ns() : 0;
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
+          if (args.trace) tr_empty += globaltimer_ns() - te0;
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
           const uint32_t sb = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * Cfg::BK;
@@ -289,12 +296,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         const int acc = j % Cfg::NBUF;
         const uint32_t use = (uint32_t)(j / Cfg::NBUF);
+        const uint64_t tt0 = args.trace ? globaltimer_ns() : 0;
         if (!(CG == 2 ? mbar_wait_cluster(tempty_bar(acc), (use & 1u) ^ 1u, err, 2)
                       : mbar_wait(tempty_bar(acc), (use & 1u) ^ 1u, err, 2))) { ok = false; break; }
+        if (args.trace) tr_tempty += globaltimer_ns() - tt0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * Cfg::TILE_N);
         for (int kb = kb0; kb < kb1; ++kb) {
+          const uint64_t tf0 = args.trace ? globaltimer_ns() : 0;
           if (!mbar_wait(full_bar(stage), phase, err, 3)) { ok = false; break; }
+          if (args.trace) tr_full += globaltimer_ns() - tf0;
           tc_fence_after();
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
           const uint32_t sb = sB + stage * Cfg::B_BYTES;
@@ -356,7 +367,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       sched.tile_coords(t, tm, tn);
       const int acc = j % Cfg::NBUF;
       const uint32_t use = (uint32_t)(j / Cfg::NBUF);
+      const uint64_t tq0 = args.trace ? globaltimer_ns() : 0;
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
+      if (args.trace) tr_tfull += globaltimer_ns() - tq0;
       tc_fence_after();
       const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
@@ -447,6 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<CG>(tmem_base, 512);
+  if (args.trace) {
+    unsigned long long* tr = args.trace + (size_t)blockIdx.x * 8;
+    if (warp == 0 && lane == 0) { tr[0] = tr_barrier; tr[1] = tr_empty; }
+    if (warp == 1 && lane == 0) { tr[2] = tr_tempty; tr[3] = tr_full; tr[6] = tr_t0; tr[7] = globaltimer_ns(); }
+    if (warp == 2 && lane == 0) tr[4] = tr_tfull;
+  }
   // the last CTA to finish resets the wave-barrier counters for the next launch
   if (args.wave_sync && threadIdx.x == 0) {
     __threadfence();

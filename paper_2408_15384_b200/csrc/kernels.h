@@ -21,6 +21,7 @@ struct GemmArgs {
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
   int l2_hint;      // tcgen05 kernel: TMA loads of A evict_last, of B evict_first
+  unsigned long long* trace;  // optional per-CTA wait-time counters (8 per CTA), MM_TRACE=1
 };
 
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).

@@ -171,6 +171,14 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;
+  a.trace = nullptr;
+  const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
+  if (trace) {
+    if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 8 * sizeof(unsigned long long)) != cudaSuccess)
+      return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
+    cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
+    a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
+  }
   if (const char* env = getenv("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
   // stream-K workspace (partial tiles) + self-resetting per-tile counters, shared by both kernels
   auto ensure_sk = [&](size_t ws_bytes, size_t flag_count) -> mm_status {
@@ -237,6 +245,33 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     e = launch_gemm_tc(i8, cg, nt, tmA, tmB, tmC, a, ctx->num_sms, s);
   }
   if (e == cudaSuccess) ++ctx->launches;
+  if (e == cudaSuccess && trace) {
+    // CTA-average wait times by role, as fractions of the kernel's span (stderr)
+    std::vector<unsigned long long> h(4096 * 8);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), ctx->trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double sum[5] = {0, 0, 0, 0, 0};
+    int nct = 0, nmma = 0;
+    for (int c = 0; c < 4096; ++c) {
+      const unsigned long long* r = &h[(size_t)c * 8];
+      if (r[6]) {
+        t0 = std::min(t0, r[6]);
+        t1 = std::max(t1, r[7]);
+        ++nmma;
+      }
+      if (r[0] || r[1] || r[4]) ++nct;
+      for (int k = 0; k < 5; ++k) sum[k] += (double)r[k];
+    }
+    const double span = (double)(t1 - t0);
+    if (nct && nmma && span > 0)
+      fprintf(stderr,
+              "[mm trace] m=%lld n=%lld p=%lld span %.1f us | producer: wave-barrier %.2f%% empty-slot %.2f%% | "
+              "MMA: tmem-free %.2f%% smem-full %.2f%% | epilogue: tmem-ready %.2f%%\n",
+              (long long)m, (long long)n, (long long)p, span / 1e3, 100 * sum[0] / nct / span,
+              100 * sum[1] / nct / span, 100 * sum[2] / nmma / span, 100 * sum[3] / nmma / span,
+              100 * sum[4] / nct / span);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     return set_err(ctx, MM_ERR_RUNTIME, "kernel launch failed (m=%lld n=%lld p=%lld dtype=%d): %s", (long long)m,
@@ -336,6 +371,7 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_flags) cudaFree(ctx->sk_flags);
+  if (ctx->trace_buf) cudaFree(ctx->trace_buf);
   for (auto& b : ctx->hbuf)
     if (b) cudaFree(b);
   for (auto& b : ctx->sbuf)
