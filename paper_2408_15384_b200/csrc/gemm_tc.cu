@@ -35,7 +35,7 @@ namespace {
 constexpr int kThreads = 192;
 constexpr int kBN = 256;  // MMA N (columns of C per tile)
 
-template <bool I8, int CG, int NT>
+template <bool I8, int CG, int NT, int MC = 1>
 struct TcCfg {
   static constexpr int ESZ = I8 ? 1 : 2;
   static constexpr int BK = 128 / ESZ;        // K elements per stage (one 128-B swizzle atom)
@@ -56,6 +56,11 @@ struct TcCfg {
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr int M_MMA = 128 * CG;
+  // MC = 2: a cluster of two CTA pairs stacked along M (tile M_MMA*MC rows) shares every B slab:
+  // each pair loads half of the slab's K rows and multicasts them into both pairs' shared memory.
+  static constexpr int M_TILE = M_MMA * MC;
+  static constexpr int BKB = BK / MC;               // K rows per TMA box of B
+  static constexpr int B_PART = BOX_BYTES / MC;     // bytes of one such box
   // Instruction descriptor: c_format [4,6), a_format [7,10), b_format [10,13),
   // a_major [15] = K, b_major [16] = MN, N>>3 at [17,23), M>>4 at [24,29).
   static constexpr uint32_t IDESC = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
@@ -165,11 +170,11 @@ __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict
   add_words<I8>(v, w);
 }
 
-template <bool I8, int CG, int NT>
+template <bool I8, int CG, int NT, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
-  using Cfg = TcCfg<I8, CG, NT>;
+  using Cfg = TcCfg<I8, CG, NT, MC>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment (SWIZZLE_128B atoms) of the operand ring.
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -189,7 +194,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // rank in the cluster (CG*MC CTAs)
+  const uint32_t rank = crank & (uint32_t)(CG - 1);            // rank in the CTA pair
+  const uint32_t pair = crank / (uint32_t)CG;                   // pair index along M (MC = 2)
+  const uint32_t leader = crank - rank;                         // the pair's MMA-issuing CTA
   const int cl = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
   const int num_kb = sched.num_kb;
   int* err = args.err;
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (args.c_tma) tma_prefetch_desc(&tmC);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), MC);  // one commit from the leader of every pair reading this slot
     }
     for (int a = 0; a < Cfg::NBUF; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (args.trace) tr_barrier += globaltimer_ns() - tb0;
         int tm, tn;
         sched.tile_coords(t, tm, tn);
-        const int m0 = tm * Cfg::M_MMA + (int)rank * Cfg::BM;
+        const int m0 = tm * Cfg::M_TILE + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = tn * Cfg::TILE_N + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
         for (int kb = kb0; kb < kb1; ++kb) {
           const uint64_t te0 = args.trace ? globaltimer_ns() : 0;
@@ -264,6 +272,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
                             n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0);
             }
+          } else if constexpr (MC == 2) {
+            // A: this CTA's own 128 rows.  B: this pair's half of the K rows of each box, multicast
+            // to the same-rank CTA of both pairs (which need the same B columns).
+            const uint32_t leader_full = mapa_shared(full_bar(stage), leader);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+            const uint16_t mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+#pragma unroll
+            for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
+              tma_load_2d_pair_mc(sb + rb * Cfg::BOX_BYTES + pair * Cfg::B_PART, &tmB, leader_full,
+                                  n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN,
+                                  k0 + (int)pair * Cfg::BKB, mask);
           } else {
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
@@ -321,11 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (kb != kb0 || kk != 0) ? 1u : 0u);
             }
           }
-          tc_commit<CG>(empty_bar(stage));  // frees this smem stage (both CTAs) when the MMAs retire
+          // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
+          // in the other pair, whose producers multicast into this pair's slots
+          tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
         if (!ok) break;
-        tc_commit<CG>(tfull_bar(acc));  // accumulator ready for the epilogue (both CTAs)
+        tc_commit<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs of the pair)
       }
     }
   } else {
@@ -371,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       if (args.trace) tr_tfull += globaltimer_ns() - tq0;
       tc_fence_after();
-      const int64_t row = (int64_t)tm * Cfg::M_MMA + rank * Cfg::BM + prow;
+      const int64_t row = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
       const bool whole = (kb0 == 0 && kb1 == num_kb);
       const int tail_c = cl;  // tail items: cluster index == tail-slot index
@@ -386,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else if (kb0 != 0) {
         // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
-        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * CG + rank) * (128 * Cfg::TILE_N));
+        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * (CG * MC) + crank) * (128 * Cfg::TILE_N));
 #pragma unroll 1
         for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
           uint32_t v[32];
@@ -398,21 +420,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * CG + rank, 1u);
+        if (q == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * (CG * MC) + crank, 1u);
       } else {
         // finisher (holds k-block 0): wait for the contributors, add their slabs in cluster order
         const int64_t ti_last = (int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1;
         const int c_last = sched.tail_cluster_of(ti_last);
         if (q == 0 && lane == 0) {
-          if (counter_wait(args.flags + (size_t)t * CG + rank, (unsigned)(c_last - tail_c), err, 6))
-            *(volatile unsigned*)(args.flags + (size_t)t * CG + rank) = 0u;  // reset for the next launch
+          if (counter_wait(args.flags + (size_t)t * (CG * MC) + crank, (unsigned)(c_last - tail_c), err, 6))
+            *(volatile unsigned*)(args.flags + (size_t)t * (CG * MC) + crank) = 0u;  // reset for the next launch
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (sched.land && c_last == tail_c + 1) {
           // Exact-halves split: this is the cluster's last item, so its operand ring is idle
           // (all loads consumed, all MMAs retired).  Land the partner's slab there with one
           // 4-KB bulk copy per chunk (all in flight at once), then add it from shared memory.
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(part + ((size_t)c_last * CG + rank) * (128 * Cfg::TILE_N));
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(part + ((size_t)c_last * (CG * MC) + crank) * (128 * Cfg::TILE_N));
           if (lane == 0) {
             mbar_arrive_expect_tx(land_bar((int)q), (Cfg::TILE_N / 32) * 4096u);
             for (int c = 0; c < Cfg::TILE_N / 32; ++c)
@@ -439,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32x32b_x32(t_row + c * 32, v);
             tmem_ld_wait();
             for (int qq = tail_c + 1; qq <= c_last; ++qq)
-              add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * CG + rank) * (128 * Cfg::TILE_N)) +
+              add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * (CG * MC) + crank) * (128 * Cfg::TILE_N)) +
                                slab_index(c, (int)q, 0, (int)lane));
             emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
           }
@@ -448,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), leader));
         else mbar_arrive(tempty_bar(acc));
       }
     }
@@ -476,20 +498,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-WorkSched make_sched(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, int num_sms) {
-  const int m_mma = 128 * cg;
+// max_clusters: how many clusters of cg*mc CTAs can be co-resident (the persistent grid and the
+// wave barrier need all of them resident at once); <= 0: num_sms / (cg*mc).
+WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, int max_clusters) {
+  const int m_mma = 128 * cg * mc;
   const int bk = i8 ? 128 : 64;
   WorkSched s;
   s.tiles_m = (int)((M + m_mma - 1) / m_mma);
   s.tiles_n = (int)((N + kBN * nt - 1) / (kBN * nt));
   // measured best (tools/sweep_raster.py): 256-wide tiles 8 tile-rows x ~9 tile-cols per 74-cluster wave;
   // 512-wide tiles 16 x ~4.6
-  s.group_m = nt == 2 ? 16 : 8;
+  s.group_m = (nt == 2 ? 16 : 8) / mc;
   if (const char* e = getenv("MM_GROUP_M")) s.group_m = atoi(e) > 0 ? atoi(e) : s.group_m;  // tuning knob
   if (s.group_m > s.tiles_m) s.group_m = s.tiles_m;
   s.num_kb = (int)((K + bk - 1) / bk);
   const int64_t T = (int64_t)s.tiles_m * s.tiles_n;
-  int64_t nc = num_sms / cg;
+  int64_t nc = num_sms / (cg * mc);
+  if (max_clusters > 0) nc = std::min<int64_t>(nc, max_clusters);
   nc = std::min<int64_t>(nc, T * 4);  // at most ~4 clusters share one tile
   s.nc = (int)std::max<int64_t>(1, nc);
   s.W = (int)(T / s.nc);
@@ -503,8 +528,9 @@ WorkSched make_sched(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, i
   // the general split (partials read from global memory), MM_STREAMK=0 disables both.
   // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
   // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
-  int mode = (!i8 && tail > 0 && nt == 1 && 2 * tail <= s.nc && s.num_kb >= 8) ? 2 : 0;
+  int mode = (!i8 && tail > 0 && nt == 1 && mc == 1 && 2 * tail <= s.nc && s.num_kb >= 8) ? 2 : 0;
   if (const char* e = getenv("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
+  if (mc != 1) mode = 0;  // (cluster-pair multicast: whole tiles only)
   s.land = 0;
   if (mode == 0) {
     // no stream-K tail: the last partial wave runs whole tiles
@@ -523,61 +549,108 @@ WorkSched make_sched(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, i
   return s;
 }
 
-template <bool I8, int CG, int NT>
-cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
-                        int num_sms, cudaStream_t s) {
-  using Cfg = TcCfg<I8, CG, NT>;
-  auto kern = gemm_tc_kernel<I8, CG, NT>;
+template <bool I8, int CG, int NT, int MC>
+cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int num_sms, int* max_clusters) {
+  using Cfg = TcCfg<I8, CG, NT, MC>;
+  auto kern = gemm_tc_kernel<I8, CG, NT, MC>;
   static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const WorkSched sched = make_sched(I8, CG, NT, a.M, a.N, a.K, num_sms);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(sched.nc * CG, 1, 1);
+  static int max_cl = 0;
+  cfg = {};
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * MC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, a, sched);
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    // all clusters of the persistent grid must be resident together (wave barrier, stream-K waits)
+    cfg.gridDim = dim3((unsigned)(num_sms / (CG * MC) * CG * MC), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    max_cl = n;
+    attr_set = true;
+  }
+  *max_clusters = max_cl;
+  return cudaSuccess;
+}
+
+template <bool I8, int CG, int NT, int MC>
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
+                        int num_sms, cudaStream_t s) {
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  int max_cl = 0;
+  cudaError_t e = launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl);
+  if (e != cudaSuccess) return e;
+  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl);
+  cfg.gridDim = dim3(sched.nc * CG * MC, 1, 1);
+  cfg.stream = s;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC>, tmA, tmB, tmC, a, sched);
+}
+
+template <bool I8, int CG, int NT, int MC>
+int max_clusters_of(int num_sms) {
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  int max_cl = 0;
+  if (launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl) != cudaSuccess) return 0;
+  return max_cl;
+}
+
+int max_clusters_impl(bool i8, int cg, int nt, int mc, int num_sms) {
+  if (cg == 1) return i8 ? max_clusters_of<true, 1, 1, 1>(num_sms) : max_clusters_of<false, 1, 1, 1>(num_sms);
+  if (mc == 2) {
+    if (i8) return nt == 2 ? max_clusters_of<true, 2, 2, 2>(num_sms) : max_clusters_of<true, 2, 1, 2>(num_sms);
+    return nt == 2 ? max_clusters_of<false, 2, 2, 2>(num_sms) : max_clusters_of<false, 2, 1, 2>(num_sms);
+  }
+  if (i8) return nt == 2 ? max_clusters_of<true, 2, 2, 1>(num_sms) : max_clusters_of<true, 2, 1, 1>(num_sms);
+  return nt == 2 ? max_clusters_of<false, 2, 2, 1>(num_sms) : max_clusters_of<false, 2, 1, 1>(num_sms);
 }
 
 }  // namespace
 
-void tc_box_dims(bool i8, int cg, uint32_t* a_box, uint32_t* b_box) {
+int max_clusters(bool i8, int cg, int nt, int mc, int num_sms) { return max_clusters_impl(i8, cg, nt, mc, num_sms); }
+
+void tc_box_dims(bool i8, int cg, int mc, uint32_t* a_box, uint32_t* b_box) {
   const uint32_t esz = i8 ? 1 : 2;
-  a_box[0] = 128 / esz;  // K elements (128 B)
-  a_box[1] = 128;        // rows
-  b_box[0] = 128 / esz;  // N elements (128 B)
-  b_box[1] = 128 / esz;  // K rows (BK)
+  a_box[0] = 128 / esz;       // K elements (128 B)
+  a_box[1] = 128;             // rows
+  b_box[0] = 128 / esz;       // N elements (128 B)
+  b_box[1] = 128 / esz / mc;  // K rows (BK, or the half of it one pair loads when two pairs share B)
   (void)cg;
 }
 
-void tc_plan_needs(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
+void tc_plan_needs(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
                    size_t* flag_count) {
-  const WorkSched sc = make_sched(i8, cg, nt, M, N, K, num_sms);
-  *ws_bytes = (size_t)sc.ntc * cg * 128 * kBN * nt * 4;
-  *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg;
+  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, num_sms));
+  *ws_bytes = (size_t)sc.ntc * cg * mc * 128 * kBN * nt * 4;
+  *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc;
 }
 
-cudaError_t launch_gemm_tc(bool i8, int cg, int nt, const CUtensorMap& tmA, const CUtensorMap& tmB,
+cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s) {
-  if (i8) {
-    if (cg == 1) return launch_impl<true, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
-    return nt == 2 ? launch_impl<true, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
-                   : launch_impl<true, 2, 1>(tmA, tmB, tmC, a, num_sms, s);
+  if (cg == 1)
+    return i8 ? launch_impl<true, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s)
+              : launch_impl<false, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+  if (mc == 2) {
+    if (i8)
+      return nt == 2 ? launch_impl<true, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
+                     : launch_impl<true, 2, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
+    return nt == 2 ? launch_impl<false, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
+                   : launch_impl<false, 2, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
   }
-  if (cg == 1) return launch_impl<false, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
-  return nt == 2 ? launch_impl<false, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
-                 : launch_impl<false, 2, 1>(tmA, tmB, tmC, a, num_sms, s);
+  if (i8)
+    return nt == 2 ? launch_impl<true, 2, 2, 1>(tmA, tmB, tmC, a, num_sms, s)
+                   : launch_impl<true, 2, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+  return nt == 2 ? launch_impl<false, 2, 2, 1>(tmA, tmB, tmC, a, num_sms, s)
+                 : launch_impl<false, 2, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
 }
 
 }  // namespace mmb

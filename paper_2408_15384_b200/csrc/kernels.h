@@ -35,13 +35,16 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms);
 // BF16 (A,B bf16 -> C f32) and INT8 (A,B s8 -> C s32) on tcgen05.
 // tmA: dims {K, M} box {128 B of K, 128 rows}; tmB: dims {N, K} box {128 B of N, BK rows}; both SWIZZLE_128B.
 // nt: accumulators of N=256 per tile (1: 256-wide tiles, TMEM double-buffered; 2: 512-wide tiles, CG=2 only).
-cudaError_t launch_gemm_tc(bool i8, int cg, int nt, const CUtensorMap& tmA, const CUtensorMap& tmB,
+// mc: CTA pairs per cluster sharing B (2: clusters of 4 CTAs, 512-row tiles, B slabs multicast; CG=2 only).
+cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s);
 // Workspace (stream-K partial slabs) and per-tile counters the launch will use.
-void tc_plan_needs(bool i8, int cg, int nt, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
+void tc_plan_needs(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
                    size_t* flag_count);
 // Box extents the tensor maps must be encoded with.
-void tc_box_dims(bool i8, int cg, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
+void tc_box_dims(bool i8, int cg, int mc, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
+// Co-resident clusters of the given configuration (0 if the query failed).
+int max_clusters(bool i8, int cg, int nt, int mc, int num_sms);
 
 // FP64 on DMMA (mma.sync m8n8k4) with TMA-fed smem ring.
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,

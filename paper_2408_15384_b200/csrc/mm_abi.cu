@@ -173,6 +173,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.l2_hint = 0;
   a.trace = nullptr;
   const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
+  int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
     if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 8 * sizeof(unsigned long long)) != cudaSuccess)
       return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
@@ -221,11 +222,14 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     // L2->SM bytes and DRAM re-reads per FLOP, at the price of no TMEM double-buffering.
     int nt = (cg == 2 && a.wave_sync) ? 2 : 1;
     if (const char* env = getenv("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    // two CTA pairs per cluster sharing (multicasting) every B slab
+    int mc = 1;
+    if (const char* env = getenv("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     size_t ws_bytes = 0, flag_count = 0;
-    tc_plan_needs(i8, cg, nt, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
+    tc_plan_needs(i8, cg, nt, mc, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
     mm_status st = ensure_sk(ws_bytes, flag_count);
     if (st != MM_OK) return st;
-    tc_box_dims(i8, cg, abox, bbox);
+    tc_box_dims(i8, cg, mc, abox, bbox);
     const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
     if (st != MM_OK) return st;
@@ -242,7 +246,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
                      cbox, "C");
       if (st != MM_OK) return st;
     }
-    e = launch_gemm_tc(i8, cg, nt, tmA, tmB, tmC, a, ctx->num_sms, s);
+    e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, a, ctx->num_sms, s);
+    trace_nt = nt;
+    trace_mc = mc;
+    if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, ctx->num_sms);
   }
   if (e == cudaSuccess) ++ctx->launches;
   if (e == cudaSuccess && trace) {
@@ -266,9 +273,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     const double span = (double)(t1 - t0);
     if (nct && nmma && span > 0)
       fprintf(stderr,
-              "[mm trace] m=%lld n=%lld p=%lld span %.1f us | producer: wave-barrier %.2f%% empty-slot %.2f%% | "
+              "[mm trace] m=%lld n=%lld p=%lld nt=%d mc=%d mma-issuing CTAs %d (max resident clusters %d) span %.1f us | producer: wave-barrier %.2f%% empty-slot %.2f%% | "
               "MMA: tmem-free %.2f%% smem-full %.2f%% | epilogue: tmem-ready %.2f%%\n",
-              (long long)m, (long long)n, (long long)p, span / 1e3, 100 * sum[0] / nct / span,
+              (long long)m, (long long)n, (long long)p, trace_nt, trace_mc, nmma, trace_maxcl, span / 1e3, 100 * sum[0] / nct / span,
               100 * sum[1] / nct / span, 100 * sum[2] / nmma / span, 100 * sum[3] / nmma / span,
               100 * sum[4] / nct / span);
   }

@@ -188,6 +188,18 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
+// Same, multicast: the box lands at offset `dst` in every CTA of `cta_mask`, and each destination's
+// bytes are counted on the barrier at `bar_cluster`'s offset in the leader (even) CTA of that
+// destination's pair (the pair leader addressed with its peer bit clear).
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0,
+                                                    int32_t c1, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+
 // 1-D bulk copy global -> this CTA's smem (16-B aligned, size a multiple of 16), completion on `bar`.
 __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),

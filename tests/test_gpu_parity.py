@@ -198,6 +198,39 @@ def test_wide_tiles_nt2(mm, dt, streamk):
         os.environ.pop("MM_STREAMK", None)
 
 
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+@pytest.mark.parametrize("nt", ["1", "2"])
+def test_cluster_multicast_mc2(mm, dt, nt):
+    """Clusters of two CTA pairs (512-row tiles) sharing every B slab by TMA multicast, each
+    pair loading half of its K rows: ragged m (partial second pair), ragged n and p, and a
+    guard-banded C (no store outside C)."""
+    os.environ["MM_MC"] = "2"
+    os.environ["MM_NT"] = nt
+    try:
+        for (m, n, p) in [(300, 200, 520), (513, 1024, 1100), (1100, 768, 1700), (2048, 2048, 2048), (777, 64, 300)]:
+            A, B = gen(dt, "exact", 44, m, n, p, 255 if dt == "i8" else 9)
+            Cref, D = ref(dt, A, B)
+            check(dt, run_gpu(mm, A, B, dt, 2), Cref, D, exact=True)
+        A, B = gen(dt, "random", 45, 1100, 768, 1700)
+        Cref, D = ref(dt, A, B)
+        check(dt, run_gpu(mm, A, B, dt, 2), Cref, D, exact=False)
+        out = torch.float32 if dt == "bf16" else torch.int32
+        m, n, p = 900, 512, 700
+        A, B = gen(dt, "exact", 46, m, n, p, 255 if dt == "i8" else 9)
+        Cref, _ = ref(dt, A, B)
+        guard = 4096
+        buf = torch.full((guard + m * p + guard,), -7, dtype=out, device="cuda")
+        C = buf[guard:guard + m * p].view(m, p)
+        mm.gemm(to_dev(A, dt), to_dev(B, dt), out=C)
+        mm.sync_check()
+        h = buf.cpu().numpy()
+        assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7)
+        assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64))
+    finally:
+        os.environ.pop("MM_MC", None)
+        os.environ.pop("MM_NT", None)
+
+
 @pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
 def test_random_values_ragged(mm, dt):
     for cg in ((1, 2) if dt != "f64" else (None,)):
