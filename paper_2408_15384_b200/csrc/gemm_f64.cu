@@ -8,18 +8,19 @@
 // producer warp and eight consumer warps ("cache tiling",
 // PAPER.md:366-373 prefetching/pipelining, done by TMA instead of the CPU).
 //
-// Work split: "stream-K".  The (tile, k-block) iteration space is cut into
-// gridDim.x equal contiguous ranges, one per persistent CTA, so every SM gets
-// the same number of DMMA k-blocks whatever the tile count (no partial last
-// wave: C2's 224 tiles on 148 SMs, C1's 16 small tiles).  A tile whose k-range
-// spans several CTAs is finished by the CTA holding its k-block 0 (always the
-// last segment of that CTA's range): the other contributors (whose segment is
-// the first of their range) publish partial tiles to a workspace and bump a
-// per-tile counter; the finisher adds them in CTA order — a fixed order, so
-// results are deterministic run to run.
+// Work split (sched.cuh): whole tiles in grouped-raster waves over the persistent
+// CTAs (concurrent tiles share A row panels and B column panels in L2), then the
+// tiles of the last, partial wave split "stream-K" style over all CTAs, so every
+// SM gets the same number of DMMA k-blocks (C2: 224 tiles on 148 SMs = 1 wave +
+// an even tail).  A split tile is finished by the CTA holding its k-block 0; the
+// other contributors publish partial tiles to a workspace and bump a per-tile
+// counter; the finisher adds them in CTA order — a fixed order, so results are
+// deterministic run to run.
 //
-// CTA tile BM×BN (128×128, or 64×64 for small problems), K slab 16 (one 128-B
-// swizzle row of A).  Consumer warp w owns a (BM/2)×(BN/4) sub-tile.
+// CTA tile BM×BN (128×128; 64×64 or 32×32 for small problems, where 32×32 tiles
+// give every CTA one whole tile and no fix-up: C1 = 64 tiles), K slab 16 (one
+// 128-B swizzle row of A).  WM×WN consumer warps, each owning a (BM/WM)×(BN/WN)
+// sub-tile.
 // Fragment loads are conflict-free with the swizzle because each DMMA's four
 // k indices are taken from rows {b, b+1, b+4, b+5} of the slab (b ∈ {0,2,8,10}):
 // the same four k's for A and B, so each DMMA still adds A[i][k]·B[k][j] over
@@ -27,6 +28,7 @@
 // Edges: TMA zero-fills out-of-bounds reads; stores are predicated.
 #include "kernels.h"
 #include "ptx.cuh"
+#include "sched.cuh"
 
 namespace mmb {
 
@@ -35,36 +37,29 @@ namespace {
 constexpr int BK = 16;
 constexpr int STAGES = 6;
 constexpr int BBOX_BYTES = BK * 16 * 8;  // 2 KB, box {16 cols, 16 rows}
-constexpr int NCONS = 8;                  // consumer warps
-constexpr int kThreads = (NCONS + 1) * 32;
 
-template <int BM, int BN>
+template <int BM, int BN, int WM, int WN>
 struct F64Cfg {
+  static constexpr int NCONS = WM * WN;        // consumer warps
+  static constexpr int THREADS = (NCONS + 1) * 32;
   static constexpr int A_BYTES = BM * BK * 8;  // one box {16, BM}
   static constexpr int NBBOX = BN / 16;
   static constexpr int B_BYTES = NBBOX * BBOX_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
-  static constexpr int MI = BM / 16;  // 8-row DMMA tiles per warp (warp rows = BM/2)
-  static constexpr int NI = BN / 32;  // 8-col DMMA tiles per warp (warp cols = BN/4)
+  static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
+  static constexpr int NI = BN / WN / 8;  // 8-col DMMA tiles per warp (even: pairs share a 16-col box)
+  static_assert(NI % 2 == 0 && MI >= 1, "warp tile");
 };
-
-__device__ __forceinline__ int64_t range_start(int c, int64_t total, int G) { return ((int64_t)c * total) / G; }
-
-__device__ __forceinline__ int cta_of(int64_t it, int64_t total, int G) {
-  int c = (int)((it * G) / total);
-  while (c + 1 < G && range_start(c + 1, total, G) <= it) ++c;
-  while (c > 0 && range_start(c, total, G) > it) --c;
-  return c;
-}
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int BM, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
-                    int tiles_m, int num_kb, int64_t total_iters) {
-  using Cfg = F64Cfg<BM, BN>;
+                    WorkSched sched) {
+  using Cfg = F64Cfg<BM, BN, WM, WN>;
+  constexpr int NCONS = Cfg::NCONS;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
@@ -77,10 +72,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int G = gridDim.x;
   const int c = blockIdx.x;
-  const int64_t it_begin = range_start(c, total_iters, G);
-  const int64_t it_end = range_start(c + 1, total_iters, G);
+  const int num_kb = sched.num_kb;
   int* err = args.err;
 
   if (warp == NCONS && lane == 0) {
@@ -99,23 +92,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = it_begin; it < it_end; ++it) {
-        const int t = (int)(it / num_kb), kb = (int)(it - (int64_t)t * num_kb);
-        const int tm = t % tiles_m, tn = t / tiles_m;  // M fastest: neighbours share B columns
-        if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) break;
-        mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
-        const int k0 = kb * BK;
-        tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, full_bar(stage), k0, tm * BM);
+      bool ok = true;
+      int t, kb0, kb1;
+      for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
+        int tm, tn;
+        sched.tile_coords(t, tm, tn);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) { ok = false; break; }
+          mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, full_bar(stage), k0, tm * BM);
 #pragma unroll
-        for (int b = 0; b < Cfg::NBBOX; ++b)
-          tma_load_2d(sB + stage * Cfg::B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), tn * BN + b * 16, k0);
-        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          for (int b = 0; b < Cfg::NBBOX; ++b)
+            tma_load_2d(sB + stage * Cfg::B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), tn * BN + b * 16, k0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
       }
     }
   } else {
     // ---------------------------------------------------------------- DMMA consumers
-    const int wm = (int)warp >> 2;  // 0..1 : rows wm*(BM/2)
-    const int wn = (int)warp & 3;   // 0..3 : cols wn*(BN/4)
+    const int wm = (int)warp / WN;  // rows wm*(BM/WM)
+    const int wn = (int)warp % WN;  // cols wn*(BN/WN)
     const int g = (int)lane >> 2;   // fragment row / column index 0..7
     const int kk = (int)lane & 3;   // fragment k index 0..3
     // Conflict-free fragment loads (LDS.64 is served per half-warp: lanes 0-15 then 16-31).
@@ -127,10 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bcol = (g & 1) + (((g >> 1) & 1) << 3) + ((g >> 2) << 1);  // B column of fragment col g
     const int dcol = ((kk & 1) << 3) + ((kk >> 1) << 1);          // first of this thread's 2 D columns
     // k = qd*4 + kk.  A: row r = wm*BM/2 + mi*8 + arow (r & 7 == arow), 16-B chunk k>>1, half k&1.
-    const int a_base0 = (wm * (BM / 2) + arow) * 128 + (kk & 1) * 8;
+    const int a_base0 = (wm * (BM / WM) + arow) * 128 + (kk & 1) * 8;
     const int a_x0 = (kk >> 1) ^ arow;
-    // B: column c16 = (ni&1)*4 + bcol in box wn*BN/64 + ni/2; chunk (c16>>1) ^ (k & 7), half c16 & 1.
-    const int b_base0 = wn * (BN / 64) * BBOX_BYTES + kk * 128 + (bcol & 1) * 8;
+    // B: column c16 = (ni&1)*4 + bcol in box wn*NI/2 + ni/2; chunk (c16>>1) ^ (k & 7), half c16 & 1.
+    const int b_base0 = wn * (Cfg::NI / 2) * BBOX_BYTES + kk * 128 + (bcol & 1) * 8;
     const int b_x0 = (bcol >> 1) ^ kk;
     double* C = reinterpret_cast<double*>(args.C);
     double* part = reinterpret_cast<double*>(args.ws);
@@ -138,13 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     bool ok = true;
-    int64_t it = it_begin;
-    while (it < it_end && ok) {
-      const int t = (int)(it / num_kb);
-      const int kb0 = (int)(it - (int64_t)t * num_kb);
-      const int64_t kb_end = (int64_t)kb0 + (it_end - it);
-      const int kb1 = kb_end < (int64_t)num_kb ? (int)kb_end : num_kb;
-      const int tm = t % tiles_m, tn = t / tiles_m;
+    int t, kb0, kb1;
+    for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
+      int tm, tn;
+      sched.tile_coords(t, tm, tn);
       double acc[Cfg::MI][Cfg::NI][2];
 #pragma unroll
       for (int mi = 0; mi < Cfg::MI; ++mi)
@@ -162,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("mov.b32 %0, %1;" : "=r"(b_x) : "r"(b_x0));
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const int k = qd * 4 + kk;
           // Fragment addresses from two thread constants re-materialised per k-block (opaque
           // to the compiler, so it does not hoist 16+ loop-invariant addresses and spill them):
           //   A: pa + a_base + (((qd<<1) ^ a_x) << 4) + mi*1024
@@ -180,6 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ni = 0; ni < Cfg::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
           }
         }
+        // The slot is refilled by TMA (async proxy) once all warps arrived: order this warp's
+        // shared-memory fragment loads (generic proxy) before that.  Without the proxy fence
+        // ptxas issued the arrive while the last A-fragment load was still in flight, and a
+        // late warp occasionally read the next k-block's data (wrong rows 56-63 of warp 0).
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_bar(stage));
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
@@ -194,8 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int r = wm * (BM / 2) + mi * 8 + arow, cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-            __stcg(reinterpret_cast<double2*>(slot + r * BN + cc), make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+            const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+            st_cg_d2(slot + r * BN + cc, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
           }
         __threadfence();
         named_bar(1, NCONS * 32);
@@ -203,12 +201,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         if (!whole) {
           // ---- finisher (holds k-block 0): wait for the other contributors, add them in CTA order
-          const int c_last = cta_of((int64_t)t * num_kb + num_kb - 1, total_iters, G);
+          const int c_last = sched.tail_cluster_of((int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1);
           const unsigned expect = (unsigned)(c_last - c);
           if (warp == 0 && lane == 0) {
             if (!counter_wait(args.flags + t, expect, err, 13)) ok = false;
             else *(volatile unsigned*)(args.flags + t) = 0u;  // reset for the next launch
           }
+          // bar.sync is .aligned: warp 0 must reconverge (lane 0 done waiting) before it arrives,
+          // else the barrier can release the other warps before the partials are acquired
+          __syncwarp();
           named_bar(1, NCONS * 32);
           for (int q = c + 1; q <= c_last; ++q) {
             const double* slot = part + (size_t)q * (BM * BN);
@@ -216,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
               for (int ni = 0; ni < Cfg::NI; ++ni) {
-                const int r = wm * (BM / 2) + mi * 8 + arow, cc = wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-                const double2 v = __ldcg(reinterpret_cast<const double2*>(slot + r * BN + cc));
+                const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+                const double2 v = ld_cg_d2(slot + r * BN + cc);
                 acc[mi][ni][0] += v.x;
                 acc[mi][ni][1] += v.y;
               }
@@ -226,11 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- epilogue: registers -> global (predicated on the ragged edges), β ∈ {0, 1}
 #pragma unroll
         for (int mi = 0; mi < Cfg::MI; ++mi) {
-          const int64_t row = (int64_t)tm * BM + wm * (BM / 2) + mi * 8 + arow;
+          const int64_t row = (int64_t)tm * BM + wm * (BM / WM) + mi * 8 + arow;
           if (row >= args.M) continue;
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int64_t col = (int64_t)tn * BN + wn * (BN / 4) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+            const int64_t col = (int64_t)tn * BN + wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
             double* dst = C + row * args.ldc + col;
             double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
             if (vec_ok && col + 1 < args.N) {
@@ -247,26 +248,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      it += kb1 - kb0;
     }
   }
   __syncwarp();
   __syncthreads();
 }
 
-template <int BM, int BN>
+template <int BM, int BN, int WM, int WN>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                         cudaStream_t s) {
-  using Cfg = F64Cfg<BM, BN>;
+  using Cfg = F64Cfg<BM, BN, WM, WN>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_f64_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  gemm_f64_kernel<BM, BN><<<pl.grid, kThreads, Cfg::SMEM_BYTES, s>>>(tmA, tmB, a, pl.tiles_m, pl.num_kb,
-                                                                      (int64_t)pl.tiles_m * pl.tiles_n * pl.num_kb);
+  kern<<<pl.sched.nc, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(tmA, tmB, a, pl.sched);
   return cudaGetLastError();
 }
 
@@ -274,18 +273,35 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
 
 F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   F64Plan pl;
-  const int64_t t128 = ((M + 127) / 128) * ((N + 127) / 128);
-  pl.bm = pl.bn = (t128 >= num_sms) ? 128 : 64;
-  pl.tiles_m = (int)((M + pl.bm - 1) / pl.bm);
-  pl.tiles_n = (int)((N + pl.bn - 1) / pl.bn);
-  pl.num_kb = (int)((K + BK - 1) / BK);
-  const int64_t total = (int64_t)pl.tiles_m * pl.tiles_n * pl.num_kb;
-  // each CTA should own >= 4 k-blocks (pipeline fill) and every tile has at most ~4 contributors
-  int64_t g = std::min<int64_t>((int64_t)num_sms, (total + 3) / 4);
-  g = std::min<int64_t>(g, (int64_t)pl.tiles_m * pl.tiles_n * 4);
-  pl.grid = (int)std::max<int64_t>(1, g);
-  pl.ws_bytes = (size_t)pl.grid * pl.bm * pl.bn * sizeof(double);
-  pl.flag_count = pl.tiles_m * pl.tiles_n;
+  auto tiles = [&](int b) { return ((M + b - 1) / b) * ((N + b - 1) / b); };
+  // 128x128 when there is at least a wave of them; else 32x32 when those fit one wave (every
+  // CTA one whole tile, no fix-up: C1 = 64 tiles); else 64x64 (measured: 512^3 20.5 us at 64x64
+  // split vs 26.6 us at 32x32 split, tools/ab_gpu.py).
+  pl.bm = pl.bn = tiles(128) >= num_sms ? 128 : (tiles(32) <= num_sms ? 32 : 64);
+  if (const char* e = getenv("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 128
+    const int v = atoi(e);
+    if (v == 32 || v == 64 || v == 128) pl.bm = pl.bn = v;
+  }
+  const int tiles_m = (int)((M + pl.bm - 1) / pl.bm);
+  const int tiles_n = (int)((N + pl.bn - 1) / pl.bn);
+  const int num_kb = (int)((K + BK - 1) / BK);
+  const int64_t T = (int64_t)tiles_m * tiles_n;
+  int64_t nc;
+  int mode;
+  if (T <= num_sms && pl.bm == 32) {
+    nc = T;  // one whole tile per CTA
+    mode = 0;
+  } else {
+    // whole-tile waves, then the partial last wave split evenly: each CTA >= 4 k-blocks,
+    // each tile at most ~4 contributors
+    nc = std::min<int64_t>((int64_t)num_sms, T * 4);
+    nc = std::min<int64_t>(nc, std::max<int64_t>(1, T * num_kb / 4));
+    mode = 1;
+  }
+  if (const char* e = getenv("MM_F64_STREAMK")) mode = atoi(e) != 0 ? 1 : 0;  // tuning knob
+  pl.sched = sched_build(tiles_m, tiles_n, 8, num_kb, (int)std::max<int64_t>(1, nc), mode);
+  pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
+  pl.flag_count = (int)T;
   return pl;
 }
 
@@ -298,8 +314,9 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
 
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                             cudaStream_t s) {
-  if (pl.bm == 128) return launch_impl<128, 128>(tmA, tmB, a, pl, s);
-  return launch_impl<64, 64>(tmA, tmB, a, pl, s);
+  if (pl.bm == 128) return launch_impl<128, 128, 2, 4>(tmA, tmB, a, pl, s);
+  if (pl.bm == 64) return launch_impl<64, 64, 2, 4>(tmA, tmB, a, pl, s);
+  return launch_impl<32, 32, 2, 2>(tmA, tmB, a, pl, s);
 }
 
 }  // namespace mmb

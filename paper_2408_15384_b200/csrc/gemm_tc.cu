@@ -27,6 +27,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "sched.cuh"
 
 namespace mmb {
 
@@ -65,65 +66,6 @@ struct TcCfg {
   // a_major [15] = K, b_major [16] = MN, N>>3 at [17,23), M>>4 at [24,29).
   static constexpr uint32_t IDESC = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                                     ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(M_MMA >> 4) << 24);
-};
-
-// Work schedule: every cluster first takes whole tiles round-robin (W full waves,
-// grouped raster), then the tiles of the last, partial wave are split stream-K
-// style: their (tile, k-block) iterations are cut into ntc equal ranges, one per
-// cluster, so no SM idles through a ragged last wave (C3: 3.46 waves -> 3 + an
-// even tail; C4: 55.35 -> 55 + tail).  A split tile is finished by the cluster
-// holding its k-block 0 (the last segment of that cluster's range); the others
-// (the first segment of theirs) publish partial tiles and bump a counter; the
-// finisher adds them in cluster order (fixed order: deterministic).
-struct WorkSched {
-  int tiles_m, tiles_n, group_m, num_kb;
-  int nc;    // clusters
-  int W;     // full data-parallel waves
-  int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
-  int land;  // tail tiles split in exact halves: the finisher lands the partner's slab in its idle stage ring
-  int64_t TI;  // tail iterations = tail tiles * num_kb
-
-  __device__ __forceinline__ void tile_coords(int t, int& tm, int& tn) const {
-    const int per_group = group_m * tiles_n;
-    const int g = t / per_group;
-    const int first_m = g * group_m;
-    const int gm = min(tiles_m - first_m, group_m);
-    const int r = t - g * per_group;
-    tm = first_m + r % gm;
-    tn = r / gm;
-  }
-  __device__ __forceinline__ int64_t tstart(int c) const { return ((int64_t)c * TI) / ntc; }
-  __device__ __forceinline__ int tail_cluster_of(int64_t it) const {
-    int c = (int)((it * ntc) / TI);
-    while (c + 1 < ntc && tstart(c + 1) <= it) ++c;
-    while (c > 0 && tstart(c) > it) --c;
-    return c;
-  }
-  // j-th work item of cluster c: tile t, k-blocks [kb0, kb1). Returns false past the end.
-  __device__ __forceinline__ bool item(int c, int j, int& t, int& kb0, int& kb1) const {
-    if (j < W) {
-      t = c + j * nc;
-      kb0 = 0;
-      kb1 = num_kb;
-      return t < tiles_m * tiles_n;
-    }
-    if (c >= ntc) return false;
-    int64_t it = tstart(c);
-    const int64_t end = tstart(c + 1);
-    for (int s = 0; it < end; ++s) {
-      const int64_t tt = it / num_kb;
-      const int k0 = (int)(it - tt * num_kb);
-      const int64_t lim = (tt + 1) * num_kb < end ? (tt + 1) * num_kb : end;
-      if (s == j - W) {
-        t = W * nc + (int)tt;
-        kb0 = k0;
-        kb1 = (int)(lim - tt * num_kb);
-        return true;
-      }
-      it = lim;
-    }
-    return false;
-  }
 };
 
 __device__ __forceinline__ void store_row32(uint32_t* __restrict__ C, int64_t ldc, int64_t row, int64_t col0,
@@ -166,7 +108,7 @@ template <bool I8>
 __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict__ src /* = slab + slab_index(c,q,0,l) */) {
   uint4 w[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = __ldcg(src + i * 32);  // 8 independent loads in flight
+  for (int i = 0; i < 8; ++i) w[i] = ld_cg_u4(src + i * 32);  // 8 independent loads in flight
   add_words<I8>(v, w);
 }
 
@@ -399,12 +341,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tail_c = cl;  // tail items: cluster index == tail-slot index
       const int64_t row_base = row - lane;  // first row of this warp's 32-row block
       if (whole) {
+        // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
+        const int64_t col0 = (int64_t)tn * Cfg::TILE_N;
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(t_row, va);
+        tmem_ld_wait();
 #pragma unroll 1
-        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c * 32, v);
+        for (int c = 0; c < Cfg::TILE_N / 32; c += 2) {
+          tmem_ld_32x32b_x32(t_row + (c + 1) * 32, vb);
+          emit(va, row_base, col0 + c * 32);
           tmem_ld_wait();
-          emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+          if (c + 2 < Cfg::TILE_N / 32) tmem_ld_32x32b_x32(t_row + (c + 2) * 32, va);
+          emit(vb, row_base, col0 + (c + 1) * 32);
+          tmem_ld_wait();
         }
       } else if (kb0 != 0) {
         // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
@@ -416,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            __stcg(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+            st_cg_u4(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
         }
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -429,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (counter_wait(args.flags + (size_t)t * (CG * MC) + crank, (unsigned)(c_last - tail_c), err, 6))
             *(volatile unsigned*)(args.flags + (size_t)t * (CG * MC) + crank) = 0u;  // reset for the next launch
         }
+        __syncwarp();  // reconverge warp q=0 before the (.aligned) named barrier
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (sched.land && c_last == tail_c + 1) {
           // Exact-halves split: this is the cluster's last item, so its operand ring is idle
@@ -436,6 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // 4-KB bulk copy per chunk (all in flight at once), then add it from shared memory.
           const uint8_t* src = reinterpret_cast<const uint8_t*>(part + ((size_t)c_last * (CG * MC) + crank) * (128 * Cfg::TILE_N));
           if (lane == 0) {
+            // the slab was written by another SM through the generic proxy and acquired above;
+            // order that before the async-proxy (bulk copy) reads of it
+            asm volatile("fence.proxy.async.global;" ::: "memory");
             mbar_arrive_expect_tx(land_bar((int)q), (Cfg::TILE_N / 32) * 4096u);
             for (int c = 0; c < Cfg::TILE_N / 32; ++c)
               bulk_copy_g2s(sA + (uint32_t)(c * 4 + q) * 4096u, src + slab_index(c, (int)q, 0, 0) * 16, 4096u,
@@ -503,23 +456,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, int max_clusters) {
   const int m_mma = 128 * cg * mc;
   const int bk = i8 ? 128 : 64;
-  WorkSched s;
-  s.tiles_m = (int)((M + m_mma - 1) / m_mma);
-  s.tiles_n = (int)((N + kBN * nt - 1) / (kBN * nt));
+  const int tiles_m = (int)((M + m_mma - 1) / m_mma);
+  const int tiles_n = (int)((N + kBN * nt - 1) / (kBN * nt));
   // measured best (tools/sweep_raster.py): 256-wide tiles 8 tile-rows x ~9 tile-cols per 74-cluster wave;
   // 512-wide tiles 16 x ~4.6
-  s.group_m = (nt == 2 ? 16 : 8) / mc;
-  if (const char* e = getenv("MM_GROUP_M")) s.group_m = atoi(e) > 0 ? atoi(e) : s.group_m;  // tuning knob
-  if (s.group_m > s.tiles_m) s.group_m = s.tiles_m;
-  s.num_kb = (int)((K + bk - 1) / bk);
-  const int64_t T = (int64_t)s.tiles_m * s.tiles_n;
+  int group_m = (nt == 2 ? 16 : 8) / mc;
+  if (const char* e = getenv("MM_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
+  const int num_kb = (int)((K + bk - 1) / bk);
+  const int64_t T = (int64_t)tiles_m * tiles_n;
   int64_t nc = num_sms / (cg * mc);
   if (max_clusters > 0) nc = std::min<int64_t>(nc, max_clusters);
-  nc = std::min<int64_t>(nc, T * 4);  // at most ~4 clusters share one tile
-  s.nc = (int)std::max<int64_t>(1, nc);
-  s.W = (int)(T / s.nc);
-  const int64_t tail = T - (int64_t)s.W * s.nc;
-  s.TI = tail * s.num_kb;
+  nc = std::max<int64_t>(1, std::min<int64_t>(nc, T * 4));  // at most ~4 clusters share one tile
+  const int64_t tail = T % nc;
   // The split tail pays for its partial-slab round trip only when there are many full waves
   // (measured: C4 55 waves +0.6 %, C3 3 waves -12 %; tools/ab_gpu.py).
   // Default: split the tail tiles into exact halves when there are enough clusters
@@ -528,25 +476,11 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // the general split (partials read from global memory), MM_STREAMK=0 disables both.
   // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
   // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
-  int mode = (!i8 && tail > 0 && nt == 1 && mc == 1 && 2 * tail <= s.nc && s.num_kb >= 8) ? 2 : 0;
+  int mode = (!i8 && tail > 0 && nt == 1 && mc == 1 && 2 * tail <= nc && num_kb >= 8) ? 2 : 0;
   if (const char* e = getenv("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
-  if (mc != 1) mode = 0;  // (cluster-pair multicast: whole tiles only)
-  s.land = 0;
-  if (mode == 0) {
-    // no stream-K tail: the last partial wave runs whole tiles
-    s.W = (int)((T + s.nc - 1) / s.nc);
-    s.ntc = 0;
-    s.TI = 0;
-  } else if (mode == 2 && nt == 1 && 2 * tail <= s.nc) {
-    s.ntc = (int)(2 * tail);  // exact halves: finisher + one contributor per tile
-    s.land = 1;
-  } else {
-    // >= 4 k-blocks per segment, <= 4 segments per tile
-    int64_t ntc = std::min<int64_t>(s.nc, tail * 4);
-    ntc = std::min<int64_t>(ntc, std::max<int64_t>(1, s.TI / 4));
-    s.ntc = (int)std::max<int64_t>(1, ntc);
-  }
-  return s;
+  if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
+  if (mode == 2 && (nt != 1 || 2 * tail > nc)) mode = 1;  // landing: 256-wide tiles, one partner per tile
+  return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)nc, mode);
 }
 
 template <bool I8, int CG, int NT, int MC>

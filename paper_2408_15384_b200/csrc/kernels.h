@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "sched.cuh"
+
 namespace mmb {
 
 // Problem as the kernels see it: C (M×N, leading dim ldc elements) = A (M×K) · B (K×N).
@@ -26,7 +28,8 @@ struct GemmArgs {
 
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).
 struct F64Plan {
-  int bm, bn, tiles_m, tiles_n, num_kb, grid;
+  int bm, bn;       // CTA tile
+  WorkSched sched;  // whole-tile waves + split tail over sched.nc persistent CTAs
   size_t ws_bytes;
   int flag_count;
 };

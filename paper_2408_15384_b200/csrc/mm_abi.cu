@@ -220,7 +220,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (!cg) cg = (m <= 128) ? 1 : 2;
     // 512-wide tiles (two N=256 accumulators per CTA pair) for large operands: 25 % fewer
     // L2->SM bytes and DRAM re-reads per FLOP, at the price of no TMEM double-buffering.
-    int nt = (cg == 2 && a.wave_sync) ? 2 : 1;
+    // ... and whenever they fill at least one wave of the pairs (measured 4096^3: int8 +3 %,
+    // bf16 +6 %; 2048^3, 32 wide tiles for 74 pairs: -25 %, tools/ab_gpu.py)
+    const int64_t tiles_nt2 = ((m + 255) / 256) * ((p + 511) / 512);
+    int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= ctx->num_sms / 2)) ? 2 : 1;
     if (const char* env = getenv("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // two CTA pairs per cluster sharing (multicasting) every B slab
     int mc = 1;

@@ -198,6 +198,50 @@ def test_wide_tiles_nt2(mm, dt, streamk):
         os.environ.pop("MM_STREAMK", None)
 
 
+@pytest.mark.parametrize("dt", ["f64", "bf16", "i8"])
+def test_split_tile_fixup_repeated(mm, dt):
+    """Race check of the split-tile fix-up (contributors publish partials, the finisher waits on
+    a counter and adds them): many back-to-back launches of split-heavy shapes, every output
+    compared bit-exactly (exact-integer inputs).  A premature release of the finisher's named
+    barrier (bar.sync by a divergent warp) showed up here as a few wrong rows in one tile."""
+    env = {"f64": {"MM_F64_TILE": "128", "MM_F64_STREAMK": "1"}, "bf16": {"MM_STREAMK": "1"},
+           "i8": {"MM_STREAMK": "1"}}[dt]
+    os.environ.update(env)
+    try:
+        for (m, n, p) in [(1100, 768, 1700), (513, 2048, 700)]:
+            A, B = gen(dt, "exact", 49, m, n, p, {"i8": 255, "bf16": 9, "f64": 2049}[dt])
+            Cref, _ = ref(dt, A, B)
+            Ad, Bd = to_dev(A, dt), to_dev(B, dt)
+            outs = [mm.gemm(Ad, Bd) for _ in range(12)]
+            mm.sync_check()
+            for C in outs:
+                assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+
+
+@pytest.mark.parametrize("tile", ["32", "64", "128"])
+@pytest.mark.parametrize("streamk", ["0", "1"])
+def test_f64_tiles_and_schedules(mm, tile, streamk):
+    """FP64 kernel at every CTA tile (32x32 / 64x64 / 128x128 with 4 / 8 / 8 DMMA warps), with
+    whole-tile waves only or with the split last wave, on ragged and multi-wave shapes; the
+    exact-integer inputs make every tile, seam and partial-tile sum bit-exact."""
+    os.environ["MM_F64_TILE"] = tile
+    os.environ["MM_F64_STREAMK"] = streamk
+    try:
+        for (m, n, p) in [(256, 256, 256), (300, 200, 520), (129, 1000, 77), (1100, 768, 1700), (2100, 300, 2050)]:
+            A, B = gen("f64", "exact", 47, m, n, p, 2049)
+            Cref, D = ref("f64", A, B)
+            check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=True)
+        A, B = gen("f64", "random", 48, 1100, 768, 1700)
+        Cref, D = ref("f64", A, B)
+        check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=False)
+    finally:
+        os.environ.pop("MM_F64_TILE", None)
+        os.environ.pop("MM_F64_STREAMK", None)
+
+
 @pytest.mark.parametrize("dt", ["i8", "bf16"])
 @pytest.mark.parametrize("nt", ["1", "2"])
 def test_cluster_multicast_mc2(mm, dt, nt):
