@@ -35,18 +35,26 @@ namespace mmb {
 namespace {
 
 constexpr int BK = 16;
-constexpr int STAGES = 6;
 constexpr int BBOX_BYTES = BK * 16 * 8;  // 2 KB, box {16 cols, 16 rows}
 
-template <int BM, int BN, int WM, int WN>
+// KS: k-block groups of WM x WN consumer warps.  KS = 2 (small tiles): the two groups take the
+// even / odd k-blocks of each tile (twice the DMMA chains in flight per SMSP), and group 1's
+// accumulators are added into group 0's through shared memory before the epilogue.
+template <int BM, int BN, int WM, int WN, int KS = 1>
 struct F64Cfg {
-  static constexpr int NCONS = WM * WN;        // consumer warps
+  static constexpr int NTILE = WM * WN;        // warps covering one tile
+  static constexpr int NCONS = NTILE * KS;     // consumer warps
   static constexpr int THREADS = (NCONS + 1) * 32;
   static constexpr int A_BYTES = BM * BK * 8;  // one box {16, BM}
   static constexpr int NBBOX = BN / 16;
   static constexpr int B_BYTES = NBBOX * BBOX_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
+  // ~200 KB of operand ring: 6 stages at 128x128, 12 at 64x64, 25 at 32x32 (a whole K <= 384 of a
+  // small tile in flight at once: the cold DRAM round trip is paid once, not K/(16*stages) times)
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 64 ? (200 * 1024) / STAGE_BYTES : 64;
+  static constexpr int SCR_BYTES = KS > 1 ? BM * BN * 8 : 0;  // group-1 accumulators
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + 1024;
+  static_assert(STAGES >= 4 && 16 * STAGES <= 1024, "ring");
   static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
   static constexpr int NI = BN / WN / 8;  // 8-col DMMA tiles per warp (even: pairs share a 16-col box)
   static_assert(NI % 2 == 0 && MI >= 1, "warp tile");
@@ -54,12 +62,14 @@ struct F64Cfg {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int BM, int BN, int WM, int WN>
-__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
+template <int BM, int BN, int WM, int WN, int KS>
+__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
                     WorkSched sched) {
-  using Cfg = F64Cfg<BM, BN, WM, WN>;
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS>;
   constexpr int NCONS = Cfg::NCONS;
+  constexpr int NTILE = Cfg::NTILE;
+  constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t base = (raw_u32 + 1023u) & ~1023u;
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), NCONS);
+      mbar_init(empty_bar(s), NTILE);  // one k-block group consumes each slot
     }
     fence_mbar_init();
   }
@@ -111,8 +121,11 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- DMMA consumers
-    const int wm = (int)warp / WN;  // rows wm*(BM/WM)
-    const int wn = (int)warp % WN;  // cols wn*(BN/WN)
+    const int kgrp = (int)warp / NTILE;          // k-block group
+    const int wm = ((int)warp % NTILE) / WN;     // rows wm*(BM/WM)
+    const int wn = ((int)warp % NTILE) % WN;     // cols wn*(BN/WN)
+    double* scr = reinterpret_cast<double*>(smem + STAGES * Cfg::STAGE_BYTES + 1024);
+    uint32_t gk = 0;  // running k-block count over this CTA's items (KS groups take gk mod KS)
     const int g = (int)lane >> 2;   // fragment row / column index 0..7
     const int kk = (int)lane & 3;   // fragment k index 0..3
     // Conflict-free fragment loads (LDS.64 is served per half-warp: lanes 0-15 then 16-31).
@@ -145,7 +158,11 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
 #pragma unroll
         for (int ni = 0; ni < Cfg::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb, ++gk) {
+        if (KS > 1 && (int)(gk % KS) != kgrp) {  // the other group's k-block
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          continue;
+        }
         if (!mbar_wait(full_bar(stage), phase, err, 12)) { ok = false; break; }
         const uint8_t* pa = smem + stage * Cfg::A_BYTES;
         const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES;
@@ -183,6 +200,32 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
       if (!ok) break;
+      if constexpr (KS > 1) {
+        // group 1 hands its partial sums to group 0 through shared memory (fixed order)
+        if (kgrp == 1) {
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              *reinterpret_cast<double2*>(scr + r * BN + cc) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            }
+        }
+        named_bar(2, NCONS * 32);
+        if (kgrp == 0) {
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              const double2 v = *reinterpret_cast<const double2*>(scr + r * BN + cc);
+              acc[mi][ni][0] += v.x;
+              acc[mi][ni][1] += v.y;
+            }
+        }
+        named_bar(3, NCONS * 32);
+        if (kgrp != 0) continue;  // group 0 finishes the tile
+      }
 
       const bool whole = (kb0 == 0 && kb1 == num_kb);
       if (!whole && kb0 != 0) {
@@ -196,7 +239,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
             st_cg_d2(slot + r * BN + cc, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
           }
         __threadfence();
-        named_bar(1, NCONS * 32);
+        named_bar(1, NTILE * 32);
         if (warp == 0 && lane == 0) red_release_gpu_add(args.flags + t, 1u);
       } else {
         if (!whole) {
@@ -210,7 +253,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
           // bar.sync is .aligned: warp 0 must reconverge (lane 0 done waiting) before it arrives,
           // else the barrier can release the other warps before the partials are acquired
           __syncwarp();
-          named_bar(1, NCONS * 32);
+          named_bar(1, NTILE * 32);
           for (int q = c + 1; q <= c_last; ++q) {
             const double* slot = part + (size_t)q * (BM * BN);
 #pragma unroll
@@ -254,11 +297,11 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN>::THREADS, 1)
   __syncthreads();
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int KS>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                         cudaStream_t s) {
-  using Cfg = F64Cfg<BM, BN, WM, WN>;
-  auto kern = gemm_f64_kernel<BM, BN, WM, WN>;
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -299,6 +342,9 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
     mode = 1;
   }
   if (const char* e = getenv("MM_F64_STREAMK")) mode = atoi(e) != 0 ? 1 : 0;  // tuning knob
+  // small tiles: two k-block groups of warps per CTA (latency-bound DMMA chains)
+  pl.ks = pl.bm == 32 ? 2 : 1;
+  if (const char* e = getenv("MM_F64_KS")) pl.ks = (pl.bm == 32 && atoi(e) == 2) ? 2 : 1;  // tuning knob
   pl.sched = sched_build(tiles_m, tiles_n, 8, num_kb, (int)std::max<int64_t>(1, nc), mode);
   pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
   pl.flag_count = (int)T;
@@ -314,9 +360,10 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
 
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
                             cudaStream_t s) {
-  if (pl.bm == 128) return launch_impl<128, 128, 2, 4>(tmA, tmB, a, pl, s);
-  if (pl.bm == 64) return launch_impl<64, 64, 2, 4>(tmA, tmB, a, pl, s);
-  return launch_impl<32, 32, 2, 2>(tmA, tmB, a, pl, s);
+  if (pl.bm == 128) return launch_impl<128, 128, 2, 4, 1>(tmA, tmB, a, pl, s);
+  if (pl.bm == 64) return launch_impl<64, 64, 2, 4, 1>(tmA, tmB, a, pl, s);
+  if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2>(tmA, tmB, a, pl, s);
+  return launch_impl<32, 32, 2, 2, 1>(tmA, tmB, a, pl, s);
 }
 
 }  // namespace mmb

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), MC);  // one commit from the leader of every pair reading this slot
     }
-    for (int a = 0; a < Cfg::NBUF; ++a) {
+    for (int a = 0; a < 2; ++a) {  // NT=1: two accumulators; NT=2: one, released in two regions
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 4 * CG);
     }
@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // optional timeline (MM_TRACE=1): per CTA ns spent waiting, by role
-  uint64_t tr_barrier = 0, tr_empty = 0, tr_tempty = 0, tr_full = 0, tr_tfull = 0;
+  uint64_t tr_barrier = 0, tr_empty = 0, tr_tempty = 0, tr_full = 0, tr_tfull = 0, tr_drain = 0;
+  uint64_t tr_c[5] = {0, 0, 0, 0, 0};  // epilogue per-chunk cycles: ld-wait, st.shared, fence, store, chunks
   const uint64_t tr_t0 = args.trace ? globaltimer_ns() : 0;
 
   if (warp == 0) {
@@ -255,34 +256,72 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       bool ok = true;
       int t, kb0, kb1;
+      // MMAs of k-block kb of this tile into accumulator region(s) [r0, r1)
+      auto issue = [&](uint32_t d_tmem, int stg, bool first_kb, int r0, int r1) {
+        const uint32_t sa = sA + stg * Cfg::A_BYTES;
+        const uint32_t sb = sB + stg * Cfg::B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
+          // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); K step = 32 B.
+          const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
+#pragma unroll
+          for (int rr = 0; rr < NT; ++rr) {
+            if (rr < r0 || rr >= r1) continue;
+            // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
+            const uint64_t bdesc =
+                umma_desc_sw128(sb + rr * Cfg::REGION_BYTES + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
+            tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (!first_kb || kk != 0) ? 1u : 0u);
+          }
+        }
+      };
+      auto wait_tempty = [&](int a, uint32_t parity) {
+        const uint64_t tt0 = args.trace ? globaltimer_ns() : 0;
+        const bool r = CG == 2 ? mbar_wait_cluster(tempty_bar(a), parity, err, 2) : mbar_wait(tempty_bar(a), parity, err, 2);
+        if (args.trace) tr_tempty += globaltimer_ns() - tt0;
+        tc_fence_after();
+        return r;
+      };
+      auto wait_full = [&](int stg, uint32_t ph) {
+        const uint64_t tf0 = args.trace ? globaltimer_ns() : 0;
+        const bool r = mbar_wait(full_bar(stg), ph, err, 3);
+        if (args.trace) tr_full += globaltimer_ns() - tf0;
+        tc_fence_after();
+        return r;
+      };
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         const int acc = j % Cfg::NBUF;
         const uint32_t use = (uint32_t)(j / Cfg::NBUF);
-        const uint64_t tt0 = args.trace ? globaltimer_ns() : 0;
-        if (!(CG == 2 ? mbar_wait_cluster(tempty_bar(acc), (use & 1u) ^ 1u, err, 2)
-                      : mbar_wait(tempty_bar(acc), (use & 1u) ^ 1u, err, 2))) { ok = false; break; }
-        if (args.trace) tr_tempty += globaltimer_ns() - tt0;
-        tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * Cfg::TILE_N);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          const uint64_t tf0 = args.trace ? globaltimer_ns() : 0;
-          if (!mbar_wait(full_bar(stage), phase, err, 3)) { ok = false; break; }
-          if (args.trace) tr_full += globaltimer_ns() - tf0;
-          tc_fence_after();
-          const uint32_t sa = sA + stage * Cfg::A_BYTES;
-          const uint32_t sb = sB + stage * Cfg::B_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
-            // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); K step = 32 B.
-            const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
-#pragma unroll
-            for (int rr = 0; rr < NT; ++rr) {
-              // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
-              const uint64_t bdesc =
-                  umma_desc_sw128(sb + rr * Cfg::REGION_BYTES + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-              tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (kb != kb0 || kk != 0) ? 1u : 0u);
-            }
+        int kb = kb0;
+        if constexpr (NT == 2) {
+          // One accumulator of two 256-column regions, released region by region by the epilogue
+          // (tempty_bar(0) / tempty_bar(1)): while region 1 of the previous tile still drains,
+          // the first STAGES k-blocks already accumulate into region 0; their slots are freed only
+          // once region 1 has consumed them too.
+          if (!wait_tempty(0, (use & 1u) ^ 1u)) { ok = false; break; }
+          const int pre = min(Cfg::STAGES, kb1 - kb0);
+          const int s0 = stage;
+          const uint32_t p0 = phase;
+          for (int i = 0; i < pre; ++i) {
+            if (!wait_full(stage, phase)) { ok = false; break; }
+            issue(d_tmem, stage, i == 0, 0, 1);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
           }
+          if (!ok || !wait_tempty(1, (use & 1u) ^ 1u)) { ok = false; break; }
+          stage = s0;
+          phase = p0;
+          for (int i = 0; i < pre; ++i) {
+            issue(d_tmem, stage, i == 0, 1, 2);
+            tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+          }
+          kb = kb0 + pre;
+        } else {
+          if (!wait_tempty(acc, (use & 1u) ^ 1u)) { ok = false; break; }
+        }
+        for (; kb < kb1; ++kb) {
+          if (!wait_full(stage, phase)) { ok = false; break; }
+          issue(d_tmem, stage, kb == kb0, 0, NT);
           // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
           // in the other pair, whose producers multicast into this pair's slots
           tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
@@ -303,26 +342,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMA store (coalesced full lines, edges clipped by the tensor map), or, when C's base/pitch
     // rule out TMA, straight from registers with predicated stores.
     uint32_t n_stores = 0;
+    // box128 (args.c_box == 128): the four epilogue warps stage their 32-row chunks into one
+    // 128-row buffer (2 x 16 KB) and one thread issues a single 128 x 32 TMA store per chunk
+    // column (4x fewer store requests); else each warp stores its own 32 x 32 box (2 x 4 KB each).
+    const bool box128 = args.c_box == 128;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0) {
       if (args.c_tma) {
-        const uint32_t buf = sEpi + ((q * 2u + (n_stores & 1u)) * 4096u);
-        if (n_stores >= 2) {
-          if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
-          __syncwarp();
+        const uint64_t c0 = args.trace ? clock64() : 0;
+        uint32_t buf;
+        if (box128) {
+          buf = sEpi + (n_stores & 1u) * 16384u + q * 4096u;  // rows q*32.. of the CTA's 128-row box
+        } else {
+          buf = sEpi + ((q * 2u + (n_stores & 1u)) * 4096u);
+          if (n_stores >= 2) {
+            if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
+            __syncwarp();
+          }
         }
+        const uint64_t c1 = args.trace ? clock64() : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
                        v[4 * i + 2], v[4 * i + 3]);
+        const uint64_t c2 = args.trace ? clock64() : 0;
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        const uint64_t c3 = args.trace ? clock64() : 0;
+        if (box128) {
+          // the issuer (warp q=0) lets nobody pass this chunk's barrier before the store issued one
+          // chunk ago has read its buffer, which the warps overwrite in the next chunk
+          if (q == 0 && lane == 0) bulk_wait_read<0>();
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (q == 0 && lane == 0) {
+            tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)(row_base - 32 * (int64_t)q));
+            bulk_commit();
+          }
+        } else if (lane == 0) {
           tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)row_base);
           bulk_commit();
+        }
+        if (args.trace) {
+          tr_c[3] += (c1 - c0) + (clock64() - c3);
+          tr_c[1] += c2 - c1;
+          tr_c[2] += c3 - c2;
+          tr_c[4] += 1;
         }
         ++n_stores;
       } else {
         store_row32(C, args.ldc, row_base + lane, col0, args.M, args.N, v, vec_ok);
+      }
+    };
+    // TMEM accumulator (NT=1) or region (NT=2) a has been read out: let the MMA warp reuse it
+    auto release = [&](int a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(tempty_bar(a), leader));
+        else mbar_arrive(tempty_bar(a));
       }
     };
     int t, kb0, kb1;
@@ -334,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t tq0 = args.trace ? globaltimer_ns() : 0;
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       if (args.trace) tr_tfull += globaltimer_ns() - tq0;
+      const uint64_t td0 = args.trace ? globaltimer_ns() : 0;  // accumulator read-out time
       tc_fence_after();
       const int64_t row = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
@@ -350,7 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < Cfg::TILE_N / 32; c += 2) {
           tmem_ld_32x32b_x32(t_row + (c + 1) * 32, vb);
           emit(va, row_base, col0 + c * 32);
+          const uint64_t w0 = args.trace ? clock64() : 0;
           tmem_ld_wait();
+          if (args.trace) tr_c[0] += clock64() - w0;
+          if (NT == 2 && c + 1 == kBN / 32 - 1) release(0);  // region 0 fully read: its MMAs may start
           if (c + 2 < Cfg::TILE_N / 32) tmem_ld_32x32b_x32(t_row + (c + 2) * 32, va);
           emit(vb, row_base, col0 + (c + 1) * 32);
           tmem_ld_wait();
@@ -420,12 +500,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), leader));
-        else mbar_arrive(tempty_bar(acc));
+      if (NT == 2) {
+        if (!whole) release(0);
+        release(1);
+      } else {
+        release(acc);
       }
+      if (args.trace) tr_drain += globaltimer_ns() - td0;
     }
     if (args.c_tma && lane == 0) bulk_wait<0>();  // all output stores complete before exit
   }
@@ -436,10 +517,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   if (warp == 1) tmem_dealloc<CG>(tmem_base, 512);
   if (args.trace) {
-    unsigned long long* tr = args.trace + (size_t)blockIdx.x * 8;
+    unsigned long long* tr = args.trace + (size_t)blockIdx.x * 16;
     if (warp == 0 && lane == 0) { tr[0] = tr_barrier; tr[1] = tr_empty; }
     if (warp == 1 && lane == 0) { tr[2] = tr_tempty; tr[3] = tr_full; tr[6] = tr_t0; tr[7] = globaltimer_ns(); }
-    if (warp == 2 && lane == 0) tr[4] = tr_tfull;
+    if (warp == 2 && lane == 0) {
+      tr[4] = tr_tfull;
+      tr[5] = tr_drain;
+      for (int k = 0; k < 5; ++k) tr[8 + k] = tr_c[k];
+    }
   }
   // the last CTA to finish resets the wave-barrier counters for the next launch
   if (args.wave_sync && threadIdx.x == 0) {

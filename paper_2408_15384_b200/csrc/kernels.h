@@ -22,6 +22,7 @@ struct GemmArgs {
   void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
+  int c_box;        // tcgen05 kernel: rows per TMA store box of C (32: one per warp, 128: one per CTA)
   int l2_hint;      // tcgen05 kernel: TMA loads of A evict_last, of B evict_first
   unsigned long long* trace;  // optional per-CTA wait-time counters (8 per CTA), MM_TRACE=1
 };
@@ -29,6 +30,7 @@ struct GemmArgs {
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).
 struct F64Plan {
   int bm, bn;       // CTA tile
+  int ks;           // k-block groups of consumer warps (2: small tiles)
   WorkSched sched;  // whole-tile waves + split tail over sched.nc persistent CTAs
   size_t ws_bytes;
   int flag_count;

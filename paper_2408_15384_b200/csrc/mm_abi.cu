@@ -168,6 +168,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ws = nullptr;
   a.flags = nullptr;
   a.c_tma = 0;
+  a.c_box = 32;
   // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;
@@ -175,9 +176,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
-    if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 8 * sizeof(unsigned long long)) != cudaSuccess)
+    if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)
       return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
-    cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 16 * sizeof(unsigned long long), s);
     a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
   }
   if (const char* env = getenv("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
@@ -243,8 +244,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     memset(&tmC, 0, sizeof tmC);
     a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
     if (const char* env = getenv("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
+    a.c_box = 32;
+    if (const char* env = getenv("MM_EPI_BOX")) a.c_box = atoi(env) == 128 ? 128 : 32;  // tuning knob
     if (a.c_tma) {
-      const uint32_t cbox[2] = {32, 32};
+      const uint32_t cbox[2] = {32, (uint32_t)a.c_box};
       st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
                      cbox, "C");
       if (st != MM_OK) return st;
@@ -257,30 +260,35 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   if (e == cudaSuccess) ++ctx->launches;
   if (e == cudaSuccess && trace) {
     // CTA-average wait times by role, as fractions of the kernel's span (stderr)
-    std::vector<unsigned long long> h(4096 * 8);
+    std::vector<unsigned long long> h(4096 * 16);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), ctx->trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull, t1 = 0;
-    double sum[5] = {0, 0, 0, 0, 0};
+    double sum[6] = {0, 0, 0, 0, 0, 0}, chunk[5] = {0, 0, 0, 0, 0};
     int nct = 0, nmma = 0;
     for (int c = 0; c < 4096; ++c) {
-      const unsigned long long* r = &h[(size_t)c * 8];
+      const unsigned long long* r = &h[(size_t)c * 16];
       if (r[6]) {
         t0 = std::min(t0, r[6]);
         t1 = std::max(t1, r[7]);
         ++nmma;
       }
       if (r[0] || r[1] || r[4]) ++nct;
-      for (int k = 0; k < 5; ++k) sum[k] += (double)r[k];
+      for (int k = 0; k < 6; ++k) sum[k] += (double)r[k];
+      for (int k = 0; k < 5; ++k) chunk[k] += (double)r[8 + k];
     }
+    if (chunk[4] > 0)
+      fprintf(stderr, "[mm trace] epilogue cycles per 4-KB chunk (warp 2): tmem-ld wait %.0f, st.shared %.0f, "
+              "proxy fence %.0f, store issue %.0f\n", chunk[0] / chunk[4], chunk[1] / chunk[4], chunk[2] / chunk[4],
+              chunk[3] / chunk[4]);
     const double span = (double)(t1 - t0);
     if (nct && nmma && span > 0)
       fprintf(stderr,
               "[mm trace] m=%lld n=%lld p=%lld nt=%d mc=%d mma-issuing CTAs %d (max resident clusters %d) span %.1f us | producer: wave-barrier %.2f%% empty-slot %.2f%% | "
-              "MMA: tmem-free %.2f%% smem-full %.2f%% | epilogue: tmem-ready %.2f%%\n",
+              "MMA: tmem-free %.2f%% smem-full %.2f%% | epilogue: tmem-ready %.2f%% read-out %.2f%%\n",
               (long long)m, (long long)n, (long long)p, trace_nt, trace_mc, nmma, trace_maxcl, span / 1e3, 100 * sum[0] / nct / span,
               100 * sum[1] / nct / span, 100 * sum[2] / nmma / span, 100 * sum[3] / nmma / span,
-              100 * sum[4] / nct / span);
+              100 * sum[4] / nct / span, 100 * sum[5] / nct / span);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();

@@ -221,13 +221,15 @@ def test_split_tile_fixup_repeated(mm, dt):
             os.environ.pop(k, None)
 
 
-@pytest.mark.parametrize("tile", ["32", "64", "128"])
+@pytest.mark.parametrize("tile", ["32", "32ks1", "64", "128"])
 @pytest.mark.parametrize("streamk", ["0", "1"])
 def test_f64_tiles_and_schedules(mm, tile, streamk):
-    """FP64 kernel at every CTA tile (32x32 / 64x64 / 128x128 with 4 / 8 / 8 DMMA warps), with
-    whole-tile waves only or with the split last wave, on ragged and multi-wave shapes; the
-    exact-integer inputs make every tile, seam and partial-tile sum bit-exact."""
-    os.environ["MM_F64_TILE"] = tile
+    """FP64 kernel at every CTA tile (32x32 with two k-block groups of 4 warps or one; 64x64 /
+    128x128 with 8 warps), with whole-tile waves only or with the split last wave, on ragged
+    and multi-wave shapes; the exact-integer inputs make every tile, seam, k-group and
+    partial-tile sum bit-exact."""
+    os.environ["MM_F64_TILE"] = tile[:2] if tile.startswith("32") else tile
+    os.environ["MM_F64_KS"] = "1" if tile == "32ks1" else "2"
     os.environ["MM_F64_STREAMK"] = streamk
     try:
         for (m, n, p) in [(256, 256, 256), (300, 200, 520), (129, 1000, 77), (1100, 768, 1700), (2100, 300, 2050)]:
@@ -239,6 +241,7 @@ def test_f64_tiles_and_schedules(mm, tile, streamk):
         check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=False)
     finally:
         os.environ.pop("MM_F64_TILE", None)
+        os.environ.pop("MM_F64_KS", None)
         os.environ.pop("MM_F64_STREAMK", None)
 
 

@@ -1,0 +1,23 @@
+// Max co-resident clusters per cluster size for a 1-CTA-per-SM kernel (227 KB smem).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/occ tools/occ_probe.cu && /tmp/occ
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void k(int* p) { extern __shared__ int s[]; if (threadIdx.x == 0 && p) p[blockIdx.x] = s[0]; }
+int main() {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs : {1, 2, 4, 6, 8, 10, 12, 16}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 16, 1, 1);
+    cfg.blockDim = dim3(192, 1, 1);
+    cfg.dynamicSmemBytes = 227 * 1024;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = cs; a[0].val.clusterDim.y = 1; a[0].val.clusterDim.z = 1;
+    cfg.attrs = a; cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, (void*)k, &cfg);
+    printf("cluster %2d: max active clusters %3d -> %3d SMs (%s)\n", cs, n, n * cs, cudaGetErrorString(e));
+  }
+  return 0;
+}
