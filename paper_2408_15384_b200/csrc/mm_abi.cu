@@ -160,7 +160,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   // The k-phase barrier pays off only when the operands do not fit in L2 (126 MB):
   // then the tiles of a wave must walk K together to share A/B slabs.
   const double operand_bytes = (double)(m * n + n * p) * (double)esz;
-  a.wave_sync = ctx->wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (ctx->wave_sync > 1);
+  int wave_sync = ctx->wave_sync;
+  if (const char* e = getenv("MM_WAVE_SYNC")) wave_sync = atoi(e);  // tuning knob (0 off, 1 auto, 2 on)
+  a.wave_sync = wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (wave_sync > 1);
 
   CUtensorMap tmA, tmB;
   uint32_t abox[2], bbox[2];
@@ -222,7 +224,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     // 512-wide tiles (two N=256 accumulators per CTA pair) for large operands: 25 % fewer
     // L2->SM bytes and DRAM re-reads per FLOP, at the price of no TMEM double-buffering.
     // ... and whenever they fill at least one wave of the pairs (measured 4096^3: int8 +3 %,
-    // bf16 +6 %; 2048^3, 32 wide tiles for 74 pairs: -25 %, tools/ab_gpu.py)
+    // bf16 +6 %; 2048^3, 32 wide tiles for 74 pairs: -25 %, tools/ab_gpu.py).  Even with a
+    // ragged last wave they win at burst clocks: the 8-GPU row block of C4 (2048 x 16384 x
+    // 16384, 3.46 waves of 512-wide tiles vs 6.92 of 256-wide ones) runs 6 % faster at NT=2.
     const int64_t tiles_nt2 = ((m + 255) / 256) * ((p + 511) / 512);
     int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= ctx->num_sms / 2)) ? 2 : 1;
     if (const char* env = getenv("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
