@@ -172,6 +172,32 @@ def per_launch_ms(fn, reps, flush_buf=None):
     return statistics.median(ts)
 
 
+def graph_us(fn, n=100, reps=5):
+    """Per-product device time of n back-to-back products replayed from one CUDA graph."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / n)
+    return statistics.median(ts)
+
+
 def per_config_table(mm, peaks):
     """Brief timings of the other BASELINE.json configs at N=1 (ours vs cuBLAS)."""
     import torch
@@ -206,8 +232,14 @@ def per_config_table(mm, peaks):
             mm.sync_check()
             t_ref = per_launch_ms(ref, reps, None if big else flush)
             tf = flops / t_ours / 1e9
+            graph = None
+            if m * n * p <= (1 << 27):
+                # launch-amortised: 100 products captured in one CUDA graph
+                graph = {"ours_us": round(graph_us(lambda: mm.gemm(A, B, out=C)), 2),
+                         "cublas_us": round(graph_us(ref), 2)}
             out[name] = {
                 "ms": round(t_ours, 4), "tflops": round(tf, 2), "frac_of_peak": round(tf / nominal, 4),
+                "graph_batch_100": graph,
                 "peak": round(nominal, 1), "peak_note": peak_note,
                 "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
                 "l2": "flushed before each launch" if not big else "operands larger than L2",
