@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t tr_barrier = 0, tr_empty = 0, tr_tempty = 0, tr_full = 0, tr_tfull = 0, tr_drain = 0;
   uint64_t tr_c[5] = {0, 0, 0, 0, 0};  // epilogue per-chunk cycles: ld-wait, st.shared, fence, store, chunks
   const uint64_t tr_t0 = args.trace ? globaltimer_ns() : 0;
+  const uint64_t tr_clk0 = args.trace ? clock64() : 0;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -191,8 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (args.trace) tr_barrier += globaltimer_ns() - tb0;
         int tm, tn;
         sched.tile_coords(t, tm, tn);
-        const int m0 = tm * Cfg::M_TILE + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
-        const int n0 = tn * Cfg::TILE_N + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
+        // (diagnostics, MM_DEBUG bit 1: every tile reads the first tile's operands -> L2 hits only)
+        const int m0 = ((args.debug & 2) ? 0 : tm * Cfg::M_TILE) + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
+        const int n0 = ((args.debug & 2) ? 0 : tn * Cfg::TILE_N) + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
         for (int kb = kb0; kb < kb1; ++kb) {
           const uint64_t te0 = args.trace ? globaltimer_ns() : 0;
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
@@ -200,7 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = sA + stage * Cfg::A_BYTES;
           const uint32_t sb = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * Cfg::BK;
-          if constexpr (CG == 1) {
+          if (args.debug & 1) {
+            // diagnostics: no operand traffic at all (MMA on whatever is in the slot)
+            if (rank == 0) mbar_arrive(full_bar(stage));
+          } else if constexpr (CG == 1) {
             mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
             if (args.l2_hint) {
               tma_load_2d_hint(sa, &tmA, full_bar(stage), k0, m0, pol_a);
@@ -519,7 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (args.trace) {
     unsigned long long* tr = args.trace + (size_t)blockIdx.x * 16;
     if (warp == 0 && lane == 0) { tr[0] = tr_barrier; tr[1] = tr_empty; }
-    if (warp == 1 && lane == 0) { tr[2] = tr_tempty; tr[3] = tr_full; tr[6] = tr_t0; tr[7] = globaltimer_ns(); }
+    if (warp == 1 && lane == 0) {
+      tr[2] = tr_tempty; tr[3] = tr_full; tr[6] = tr_t0; tr[7] = globaltimer_ns();
+      tr[13] = clock64() - tr_clk0;  // SM cycles over the CTA's life: effective clock = tr[13] / (tr[7] - tr[6])
+    }
     if (warp == 2 && lane == 0) {
       tr[4] = tr_tfull;
       tr[5] = tr_drain;

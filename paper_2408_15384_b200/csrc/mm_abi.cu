@@ -175,6 +175,8 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;
   a.trace = nullptr;
+  a.debug = 0;
+  if (const char* env = getenv("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
@@ -268,7 +270,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), ctx->trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull, t1 = 0;
-    double sum[6] = {0, 0, 0, 0, 0, 0}, chunk[5] = {0, 0, 0, 0, 0};
+    double sum[6] = {0, 0, 0, 0, 0, 0}, chunk[5] = {0, 0, 0, 0, 0}, clk_cyc = 0, clk_ns = 0;
     int nct = 0, nmma = 0;
     for (int c = 0; c < 4096; ++c) {
       const unsigned long long* r = &h[(size_t)c * 16];
@@ -276,11 +278,13 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
         t0 = std::min(t0, r[6]);
         t1 = std::max(t1, r[7]);
         ++nmma;
+        if (r[7] > r[6]) { clk_cyc += (double)r[13]; clk_ns += (double)(r[7] - r[6]); }
       }
       if (r[0] || r[1] || r[4]) ++nct;
       for (int k = 0; k < 6; ++k) sum[k] += (double)r[k];
       for (int k = 0; k < 5; ++k) chunk[k] += (double)r[8 + k];
     }
+    if (clk_ns > 0) fprintf(stderr, "[mm trace] effective SM clock during the kernel %.0f MHz\n", 1e3 * clk_cyc / clk_ns);
     if (chunk[4] > 0)
       fprintf(stderr, "[mm trace] epilogue cycles per 4-KB chunk (warp 2): tmem-ld wait %.0f, st.shared %.0f, "
               "proxy fence %.0f, store issue %.0f\n", chunk[0] / chunk[4], chunk[1] / chunk[4], chunk[2] / chunk[4],

@@ -365,6 +365,31 @@ def test_no_writes_outside_c(mm, dt):
         assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64))
 
 
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_row_blocks_bit_identical_to_full_product(mm, G):
+    """G-invariance (SURVEY 8(b) determinism): the row blocks mm_shard_range gives
+    G ranks, each multiplied on its own, reproduce the single-product C bit for bit — also for
+    random BF16 inputs, whose FP32 sums would differ under any change of summation order —
+    because no K-split is used at these shapes (tile choices differ between the full problem
+    and the blocks: 512- vs 256-wide tiles, one vs several waves)."""
+    m, n, p = 4100, 1024, 4096  # ragged last block
+    A, B = gen("bf16", "random", 60 + G, m, n, p)
+    Ad, Bd = to_dev(A, "bf16"), to_dev(B, "bf16")
+    os.environ["MM_STREAMK"] = "0"  # the contract holds without K-split (a 1025-row block would split)
+    try:
+        full = mm.gemm(Ad, Bd)
+        mm.sync_check()
+        for r in range(G):
+            r0, rows = mm.shard_range(m, G, r)
+            if rows == 0:
+                continue
+            blk = mm.gemm(Ad[r0:r0 + rows].contiguous(), Bd)
+            mm.sync_check()
+            assert torch.equal(blk, full[r0:r0 + rows]), (G, r)
+    finally:
+        os.environ.pop("MM_STREAMK", None)
+
+
 def test_determinism(mm):
     for dt in ("bf16", "f64", "i8"):
         A, B = gen(dt, "random", 12, 700, 900, 650)
