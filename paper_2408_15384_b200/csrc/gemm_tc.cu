@@ -352,7 +352,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     // column (4x fewer store requests); else each warp stores its own 32 x 32 box (2 x 4 KB each).
     const bool box128 = args.c_box == 128;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0) {
-      if (args.c_tma) {
+      if (args.c_tma && args.c_box == 0) {
+        // generic-proxy path: stage the chunk row-per-lane (128-B swizzle, conflict-free), read it
+        // back 4 rows x 8 segments per instruction and write full 128-B lines with st.global.v4
+        const uint64_t c0 = args.trace ? clock64() : 0;
+        const uint32_t buf = sEpi + q * 2u * 4096u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
+                       v[4 * i + 2], v[4 * i + 3]);
+        __syncwarp();
+        const uint64_t c1 = args.trace ? clock64() : 0;
+        const uint32_t seg = lane & 7u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t r = (uint32_t)i * 4u + (lane >> 3);  // row inside the 32-row chunk
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                       : "r"(buf + r * 128u + ((seg ^ (r & 7u)) << 4)));
+          const int64_t row = row_base + r, col = col0 + 4 * seg;
+          if (row < args.M) {
+            uint32_t* dst = C + row * args.ldc + col;
+            if (col + 4 <= args.N) {
+              asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(x0), "r"(x1), "r"(x2), "r"(x3)
+                           : "memory");
+            } else {
+              const uint32_t xs[4] = {x0, x1, x2, x3};
+              for (int u = 0; u < 4; ++u)
+                if (col + u < args.N) dst[u] = xs[u];
+            }
+          }
+        }
+        __syncwarp();  // all lanes read the staging buffer before the next chunk overwrites it
+        if (args.trace) {
+          tr_c[1] += c1 - c0;
+          tr_c[3] += clock64() - c1;
+          tr_c[4] += 1;
+        }
+      } else if (args.c_tma) {
         const uint64_t c0 = args.trace ? clock64() : 0;
         uint32_t buf;
         if (box128) {

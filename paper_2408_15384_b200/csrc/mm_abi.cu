@@ -251,9 +251,12 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
     if (const char* env = getenv("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
     a.c_box = 32;
-    if (const char* env = getenv("MM_EPI_BOX")) a.c_box = atoi(env) == 128 ? 128 : 32;  // tuning knob
+    if (const char* env = getenv("MM_EPI_BOX")) {  // tuning knob: 32 | 128 rows per TMA store, 0 = st.global
+      const int v = atoi(env);
+      a.c_box = v == 128 ? 128 : (v == 0 ? 0 : 32);
+    }
     if (a.c_tma) {
-      const uint32_t cbox[2] = {32, (uint32_t)a.c_box};
+      const uint32_t cbox[2] = {32, a.c_box == 128 ? 128u : 32u};
       st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
                      cbox, "C");
       if (st != MM_OK) return st;

@@ -390,6 +390,32 @@ def test_row_blocks_bit_identical_to_full_product(mm, G):
         os.environ.pop("MM_STREAMK", None)
 
 
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+@pytest.mark.parametrize("epi", ["32", "128", "0"])
+def test_epilogue_store_modes(mm, dt, epi):
+    """Every C store path of the tcgen05 epilogue — a TMA store per warp chunk (32), one per
+    128-row CTA chunk (128), staged st.global of full lines (0) — on ragged shapes with both
+    tile widths, inside guard bands (bit-exact, nothing written outside C)."""
+    out = torch.float32 if dt == "bf16" else torch.int32
+    os.environ["MM_EPI_BOX"] = epi
+    try:
+        for (m, n, p, nt) in [(300, 200, 520, "1"), (513, 1024, 1100, "2"), (1100, 768, 1700, "2"), (777, 64, 300, "1")]:
+            os.environ["MM_NT"] = nt
+            A, B = gen(dt, "exact", 52, m, n, p, 255 if dt == "i8" else 9)
+            Cref, _ = ref(dt, A, B)
+            guard = 4096
+            buf = torch.full((guard + m * p + guard,), -7, dtype=out, device="cuda")
+            C = buf[guard:guard + m * p].view(m, p)
+            mm.gemm(to_dev(A, dt), to_dev(B, dt), out=C)
+            mm.sync_check()
+            h = buf.cpu().numpy()
+            assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), (m, n, p, epi)
+            assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p, epi)
+    finally:
+        os.environ.pop("MM_EPI_BOX", None)
+        os.environ.pop("MM_NT", None)
+
+
 def test_determinism(mm):
     for dt in ("bf16", "f64", "i8"):
         A, B = gen(dt, "random", 12, 700, 900, 650)
