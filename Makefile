@@ -20,7 +20,7 @@ MM_HDRS := $(wildcard paper_2408_15384_b200/csrc/*.cuh) $(wildcard paper_2408_15
 GENCODE := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++17 -O3 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            -Iinclude -Ipaper_2408_15384_b200/csrc $(if $(NCCL_INC),-I$(NCCL_INC)) \
-           --expt-relaxed-constexpr -Xptxas -v
+           --expt-relaxed-constexpr -diag-suppress 177 -Xptxas -v
 
 .PHONY: all host clean
 all: $(SG_LIB) $(OR_LIB) $(MM_LIB)
