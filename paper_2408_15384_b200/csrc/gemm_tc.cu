@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
   using Cfg = TcCfg<I8, CG, NT, MC>;
+  const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
+  // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
+  unsigned long long* tl = args.trace ? args.trace + 4096 * 16 + (size_t)blockIdx.x * 32 : nullptr;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment (SWIZZLE_128B atoms) of the operand ring.
   const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t use = (uint32_t)(j / Cfg::NBUF);
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * Cfg::TILE_N);
         int kb = kb0;
+        bool tl_first = true;
         if constexpr (NT == 2) {
           // One accumulator of two 256-column regions, released region by region by the epilogue
           // (tempty_bar(0) / tempty_bar(1)): while region 1 of the previous tile still drains,
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t p0 = phase;
           for (int i = 0; i < pre; ++i) {
             if (!wait_full(stage, phase)) { ok = false; break; }
+            if (tl && i == 0 && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
             issue(d_tmem, stage, i == 0, 0, 1);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
           }
@@ -326,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (; kb < kb1; ++kb) {
           if (!wait_full(stage, phase)) { ok = false; break; }
+          if (tl && tl_first && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
           issue(d_tmem, stage, kb == kb0, 0, NT);
           // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
           // in the other pair, whose producers multicast into this pair's slots
@@ -333,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
         if (!ok) break;
+        if (tl && j < 8) tl[4 * j + 1] = globaltimer_ns();
         tc_commit<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs of the pair)
       }
     }
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
                        v[4 * i + 2], v[4 * i + 3]);
         const uint64_t c2 = args.trace ? clock64() : 0;
-        fence_proxy_async_smem();
+        if (!(args.debug & 8)) fence_proxy_async_smem();  // (diagnostics: bit 3 skips the fence)
         __syncwarp();
         const uint64_t c3 = args.trace ? clock64() : 0;
         if (box128) {
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)(row_base - 32 * (int64_t)q));
             bulk_commit();
           }
-        } else if (lane == 0) {
+        } else if (lane == 0 && !(args.debug & 4)) {  // (diagnostics: bit 2 skips the store)
           tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)row_base);
           bulk_commit();
         }
@@ -454,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       if (args.trace) tr_tfull += globaltimer_ns() - tq0;
       const uint64_t td0 = args.trace ? globaltimer_ns() : 0;  // accumulator read-out time
+      if (tl && q == 2 && lane == 0 && j < 8) tl[4 * j + 2] = td0;
       tc_fence_after();
       const int64_t row = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
@@ -550,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         release(acc);
       }
       if (args.trace) tr_drain += globaltimer_ns() - td0;
+      if (tl && q == 2 && lane == 0 && j < 8) tl[4 * j + 3] = globaltimer_ns();
     }
     if (args.c_tma && lane == 0) bulk_wait<0>();  // all output stores complete before exit
   }
@@ -565,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1 && lane == 0) {
       tr[2] = tr_tempty; tr[3] = tr_full; tr[6] = tr_t0; tr[7] = globaltimer_ns();
       tr[13] = clock64() - tr_clk0;  // SM cycles over the CTA's life: effective clock = tr[13] / (tr[7] - tr[6])
+      tr[14] = tr_entry;
     }
     if (warp == 2 && lane == 0) {
       tr[4] = tr_tfull;

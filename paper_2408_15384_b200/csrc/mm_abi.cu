@@ -180,9 +180,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
-    if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 16 * sizeof(unsigned long long)) != cudaSuccess)
+    if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
       return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
-    cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 16 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 48 * sizeof(unsigned long long), s);
     a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
   }
   if (const char* env = getenv("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
@@ -269,7 +269,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   if (e == cudaSuccess) ++ctx->launches;
   if (e == cudaSuccess && trace) {
     // CTA-average wait times by role, as fractions of the kernel's span (stderr)
-    std::vector<unsigned long long> h(4096 * 16);
+    std::vector<unsigned long long> h(4096 * 48);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), ctx->trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull, t1 = 0;
@@ -286,6 +286,35 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
       if (r[0] || r[1] || r[4]) ++nct;
       for (int k = 0; k < 6; ++k) sum[k] += (double)r[k];
       for (int k = 0; k < 5; ++k) chunk[k] += (double)r[8 + k];
+    }
+    {
+      // average timeline of the MMA-issuing CTAs, relative to the earliest kernel entry (us)
+      unsigned long long e0 = ~0ull;
+      for (int c = 0; c < 4096; ++c)
+        if (h[(size_t)c * 16 + 14]) e0 = std::min(e0, h[(size_t)c * 16 + 14]);
+      double acc[32] = {0};
+      int cnt[32] = {0};
+      double ent = 0;
+      int nent = 0;
+      for (int c = 0; c < 4096; ++c) {
+        const unsigned long long* r = &h[(size_t)c * 16];
+        const unsigned long long* tlc = &h[4096 * 16 + (size_t)c * 32];
+        if (!r[6]) continue;
+        ent += (double)(r[14] - e0);
+        ++nent;
+        for (int k = 0; k < 32; ++k)
+          if (tlc[k]) { acc[k] += (double)(tlc[k] - e0); ++cnt[k]; }
+      }
+      if (nent) {
+        fprintf(stderr, "[mm trace] timeline (us after first CTA entry, CTA average): entry %.2f", 1e-3 * ent / nent);
+        for (int j = 0; j < 8; ++j)
+          if (cnt[4 * j])
+            fprintf(stderr, " | item %d: MMA %.2f-%.2f epi %.2f-%.2f (%d)", j, 1e-3 * acc[4 * j] / cnt[4 * j],
+                    cnt[4 * j + 1] ? 1e-3 * acc[4 * j + 1] / cnt[4 * j + 1] : 0.0,
+                    cnt[4 * j + 2] ? 1e-3 * acc[4 * j + 2] / cnt[4 * j + 2] : 0.0,
+                    cnt[4 * j + 3] ? 1e-3 * acc[4 * j + 3] / cnt[4 * j + 3] : 0.0, cnt[4 * j]);
+        fprintf(stderr, "\n");
+      }
     }
     if (clk_ns > 0) fprintf(stderr, "[mm trace] effective SM clock during the kernel %.0f MHz\n", 1e3 * clk_cyc / clk_ns);
     if (chunk[4] > 0)
