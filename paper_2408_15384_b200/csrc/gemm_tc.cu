@@ -33,7 +33,7 @@ namespace mmb {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA producer, warp 1 TMEM + MMA issuer, warps 2..9 epilogue
 constexpr int kBN = 256;  // MMA N (columns of C per tile)
 
 template <bool I8, int CG, int NT, int MC = 1>
@@ -54,7 +54,7 @@ struct TcCfg {
   static constexpr int B_BYTES = NT * REGION_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (CG == 1 || NT == 2) ? 4 : 6;
-  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
+  static constexpr int EPI_BYTES = 8 * 32 * 128;  // epilogue staging: 8 warps x (32 rows x 128 B)
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr int M_MMA = 128 * CG;
   // MC = 2: a cluster of two CTA pairs stacked along M (tile M_MMA*MC rows) shares every B slab:
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
   auto land_bar = [&](int q) { return bar0 + 8u * (2 * Cfg::STAGES + 4 + q); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 8));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 12));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -155,11 +155,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), MC);  // one commit from the leader of every pair reading this slot
     }
-    for (int a = 0; a < 2; ++a) {  // NT=1: two accumulators; NT=2: one, released in two regions
-      mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4 * CG);
+    for (int a = 0; a < 2; ++a) {  // NT=1: two accumulators; NT=2: one, released region by region
+      mbar_init(tfull_bar(a), 1);   // (each release: all 8 epilogue warps of both CTAs)
+      mbar_init(tempty_bar(a), 8 * CG);
     }
-    for (int qq = 0; qq < 4; ++qq) mbar_init(land_bar(qq), 1);
+    for (int qq = 0; qq < 8; ++qq) mbar_init(land_bar(qq), 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), 512);
@@ -344,91 +344,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 2..5)
-    const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+    // ---------------------------------------------------------------- epilogue (warps 2..9)
+    // Eight warps: two per TMEM lane quarter q (warp w may only read lanes 32*(w%4)..+31) taking
+    // alternate 32-column chunks (h = 0 the even ones, h = 1 the odd ones) in column order, so for
+    // NT=2 all eight drain region 0 first and release it halfway through the read-out.
+    const uint32_t ew = warp - 2;           // epilogue warp 0..7
+    const uint32_t q = warp & 3u;           // TMEM lane quarter
+    const int h = (int)(ew >> 2);           // column half
     uint32_t* C = reinterpret_cast<uint32_t*>(args.C);
     uint32_t* part = reinterpret_cast<uint32_t*>(args.ws);
     const bool vec_ok = ((args.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.C) & 15) == 0);
     const int prow = (int)(q * 32 + lane);  // row of this thread inside the CTA's 128-row slab
-    // C tile chunk (32 rows x 32 columns) -> global: through a 128B-swizzled smem buffer and one
-    // TMA store (coalesced full lines, edges clipped by the tensor map), or, when C's base/pitch
-    // rule out TMA, straight from registers with predicated stores.
+    constexpr int NCH = Cfg::TILE_N / 32;   // 32-column chunks per accumulator
+    constexpr int HCH = NCH / 2;            // chunks per warp: c(i) = h + 2 i
+    // C chunk (32 rows x 32 columns) -> global: through this warp's 128B-swizzled 4-KB smem buffer
+    // and one TMA store (full lines, edges clipped by the tensor map), or, when C's base/pitch rule
+    // out TMA, straight from registers with predicated stores.
+    const uint32_t ebuf = sEpi + ew * 4096u;
     uint32_t n_stores = 0;
-    // box128 (args.c_box == 128): the four epilogue warps stage their 32-row chunks into one
-    // 128-row buffer (2 x 16 KB) and one thread issues a single 128 x 32 TMA store per chunk
-    // column (4x fewer store requests); else each warp stores its own 32 x 32 box (2 x 4 KB each).
-    const bool box128 = args.c_box == 128;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0) {
-      if (args.c_tma && args.c_box == 0) {
-        // generic-proxy path: stage the chunk row-per-lane (128-B swizzle, conflict-free), read it
-        // back 4 rows x 8 segments per instruction and write full 128-B lines with st.global.v4
+      if (args.c_tma) {
         const uint64_t c0 = args.trace ? clock64() : 0;
-        const uint32_t buf = sEpi + q * 2u * 4096u;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
-                       v[4 * i + 2], v[4 * i + 3]);
-        __syncwarp();
-        const uint64_t c1 = args.trace ? clock64() : 0;
-        const uint32_t seg = lane & 7u;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t r = (uint32_t)i * 4u + (lane >> 3);  // row inside the 32-row chunk
-          uint32_t x0, x1, x2, x3;
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
-                       : "r"(buf + r * 128u + ((seg ^ (r & 7u)) << 4)));
-          const int64_t row = row_base + r, col = col0 + 4 * seg;
-          if (row < args.M) {
-            uint32_t* dst = C + row * args.ldc + col;
-            if (col + 4 <= args.N) {
-              asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(x0), "r"(x1), "r"(x2), "r"(x3)
-                           : "memory");
-            } else {
-              const uint32_t xs[4] = {x0, x1, x2, x3};
-              for (int u = 0; u < 4; ++u)
-                if (col + u < args.N) dst[u] = xs[u];
-            }
-          }
-        }
-        __syncwarp();  // all lanes read the staging buffer before the next chunk overwrites it
-        if (args.trace) {
-          tr_c[1] += c1 - c0;
-          tr_c[3] += clock64() - c1;
-          tr_c[4] += 1;
-        }
-      } else if (args.c_tma) {
-        const uint64_t c0 = args.trace ? clock64() : 0;
-        uint32_t buf;
-        if (box128) {
-          buf = sEpi + (n_stores & 1u) * 16384u + q * 4096u;  // rows q*32.. of the CTA's 128-row box
-        } else {
-          buf = sEpi + ((q * 2u + (n_stores & 1u)) * 4096u);
-          if (n_stores >= 2) {
-            if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
-            __syncwarp();
-          }
+        if (n_stores >= 1) {
+          if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the buffer
+          __syncwarp();
         }
         const uint64_t c1 = args.trace ? clock64() : 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          st_shared_v4(buf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
+          st_shared_v4(ebuf + lane * 128u + ((uint32_t)(i ^ (int)(lane & 7u)) << 4), v[4 * i], v[4 * i + 1],
                        v[4 * i + 2], v[4 * i + 3]);
         const uint64_t c2 = args.trace ? clock64() : 0;
         if (!(args.debug & 8)) fence_proxy_async_smem();  // (diagnostics: bit 3 skips the fence)
         __syncwarp();
         const uint64_t c3 = args.trace ? clock64() : 0;
-        if (box128) {
-          // the issuer (warp q=0) lets nobody pass this chunk's barrier before the store issued one
-          // chunk ago has read its buffer, which the warps overwrite in the next chunk
-          if (q == 0 && lane == 0) bulk_wait_read<0>();
-          asm volatile("bar.sync 2, 128;" ::: "memory");
-          if (q == 0 && lane == 0) {
-            tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)(row_base - 32 * (int64_t)q));
-            bulk_commit();
-          }
-        } else if (lane == 0 && !(args.debug & 4)) {  // (diagnostics: bit 2 skips the store)
-          tma_store_2d(&tmC, buf, (int32_t)col0, (int32_t)row_base);
+        if (lane == 0 && !(args.debug & 4)) {  // (diagnostics: bit 2 skips the store)
+          tma_store_2d(&tmC, ebuf, (int32_t)col0, (int32_t)row_base);
           bulk_commit();
         }
         if (args.trace) {
@@ -442,7 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         store_row32(C, args.ldc, row_base + lane, col0, args.M, args.N, v, vec_ok);
       }
     };
-    // TMEM accumulator (NT=1) or region (NT=2) a has been read out: let the MMA warp reuse it
+    // TMEM accumulator (NT=1) or region (NT=2) a has been read out by this warp: let the MMA warp
+    // reuse it once all eight have
     auto release = [&](int a) {
       tc_fence_before();
       __syncwarp();
@@ -461,36 +413,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       if (args.trace) tr_tfull += globaltimer_ns() - tq0;
       const uint64_t td0 = args.trace ? globaltimer_ns() : 0;  // accumulator read-out time
-      if (tl && q == 2 && lane == 0 && j < 8) tl[4 * j + 2] = td0;
+      if (tl && ew == 0 && lane == 0 && j < 8) tl[4 * j + 2] = td0;
       tc_fence_after();
       const int64_t row = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + prow;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * Cfg::TILE_N);
       const bool whole = (kb0 == 0 && kb1 == num_kb);
       const int tail_c = cl;  // tail items: cluster index == tail-slot index
       const int64_t row_base = row - lane;  // first row of this warp's 32-row block
+      const int64_t col_t = (int64_t)tn * Cfg::TILE_N;
       if (whole) {
         // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
-        const int64_t col0 = (int64_t)tn * Cfg::TILE_N;
         uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(t_row, va);
+        tmem_ld_32x32b_x32(t_row + h * 32, va);
         tmem_ld_wait();
 #pragma unroll 1
-        for (int c = 0; c < Cfg::TILE_N / 32; c += 2) {
-          tmem_ld_32x32b_x32(t_row + (c + 1) * 32, vb);
-          emit(va, row_base, col0 + c * 32);
+        for (int i = 0; i < HCH; i += 2) {
+          const int c = h + 2 * i;  // chunks c and c + 2
+          tmem_ld_32x32b_x32(t_row + (c + 2) * 32, vb);
+          emit(va, row_base, col_t + c * 32);
           const uint64_t w0 = args.trace ? clock64() : 0;
           tmem_ld_wait();
           if (args.trace) tr_c[0] += clock64() - w0;
-          if (NT == 2 && c + 1 == kBN / 32 - 1) release(0);  // region 0 fully read: its MMAs may start
-          if (c + 2 < Cfg::TILE_N / 32) tmem_ld_32x32b_x32(t_row + (c + 2) * 32, va);
-          emit(vb, row_base, col0 + (c + 1) * 32);
+          if (i + 2 < HCH) tmem_ld_32x32b_x32(t_row + (c + 4) * 32, va);
+          emit(vb, row_base, col_t + (c + 2) * 32);
           tmem_ld_wait();
+          if (NT == 2 && i + 2 == HCH / 2) release(0);  // region 0 (chunks 0..7) read out: its MMAs may start
         }
       } else if (kb0 != 0) {
-        // contributor: publish this CTA's 128 x 256 partial slab, then signal the finisher
+        // contributor: publish this CTA's 128 x TILE_N partial slab, then signal the finisher
         uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * (CG * MC) + crank) * (128 * Cfg::TILE_N));
 #pragma unroll 1
-        for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
+        for (int c = h; c < NCH; c += 2) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
@@ -499,18 +452,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             st_cg_u4(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
         }
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * (CG * MC) + crank, 1u);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (ew == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * (CG * MC) + crank, 1u);
       } else {
         // finisher (holds k-block 0): wait for the contributors, add their slabs in cluster order
         const int64_t ti_last = (int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1;
         const int c_last = sched.tail_cluster_of(ti_last);
-        if (q == 0 && lane == 0) {
+        if (ew == 0 && lane == 0) {
           if (counter_wait(args.flags + (size_t)t * (CG * MC) + crank, (unsigned)(c_last - tail_c), err, 6))
             *(volatile unsigned*)(args.flags + (size_t)t * (CG * MC) + crank) = 0u;  // reset for the next launch
         }
-        __syncwarp();  // reconverge warp q=0 before the (.aligned) named barrier
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        __syncwarp();  // reconverge warp 0 before the (.aligned) named barrier
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (sched.land && c_last == tail_c + 1) {
           // Exact-halves split: this is the cluster's last item, so its operand ring is idle
           // (all loads consumed, all MMAs retired).  Land the partner's slab there with one
@@ -520,14 +473,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // the slab was written by another SM through the generic proxy and acquired above;
             // order that before the async-proxy (bulk copy) reads of it
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_arrive_expect_tx(land_bar((int)q), (Cfg::TILE_N / 32) * 4096u);
-            for (int c = 0; c < Cfg::TILE_N / 32; ++c)
+            mbar_arrive_expect_tx(land_bar((int)ew), HCH * 4096u);
+            for (int c = h; c < NCH; c += 2)
               bulk_copy_g2s(sA + (uint32_t)(c * 4 + q) * 4096u, src + slab_index(c, (int)q, 0, 0) * 16, 4096u,
-                            land_bar((int)q));
+                            land_bar((int)ew));
           }
-          mbar_wait(land_bar((int)q), 0u, err, 7);
+          mbar_wait(land_bar((int)ew), 0u, err, 7);
 #pragma unroll 1
-          for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
+          for (int c = h; c < NCH; c += 2) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_row + c * 32, v);
             uint4 w[8];
@@ -536,18 +489,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               w[i] = *reinterpret_cast<const uint4*>(smem + (size_t)(c * 4 + q) * 4096 + i * 512 + lane * 16);
             tmem_ld_wait();
             add_words<I8>(v, w);
-            emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+            emit(v, row_base, col_t + c * 32);
           }
         } else {
 #pragma unroll 1
-          for (int c = 0; c < Cfg::TILE_N / 32; ++c) {
+          for (int c = h; c < NCH; c += 2) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_row + c * 32, v);
             tmem_ld_wait();
             for (int qq = tail_c + 1; qq <= c_last; ++qq)
               add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * (CG * MC) + crank) * (128 * Cfg::TILE_N)) +
                                slab_index(c, (int)q, 0, (int)lane));
-            emit(v, row_base, (int64_t)tn * Cfg::TILE_N + c * 32);
+            emit(v, row_base, col_t + c * 32);
           }
         }
       }
@@ -558,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         release(acc);
       }
       if (args.trace) tr_drain += globaltimer_ns() - td0;
-      if (tl && q == 2 && lane == 0 && j < 8) tl[4 * j + 3] = globaltimer_ns();
+      if (tl && ew == 0 && lane == 0 && j < 8) tl[4 * j + 3] = globaltimer_ns();
     }
     if (args.c_tma && lane == 0) bulk_wait<0>();  // all output stores complete before exit
   }

@@ -170,7 +170,6 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ws = nullptr;
   a.flags = nullptr;
   a.c_tma = 0;
-  a.c_box = 32;
   // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;
@@ -250,13 +249,8 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     memset(&tmC, 0, sizeof tmC);
     a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
     if (const char* env = getenv("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
-    a.c_box = 32;
-    if (const char* env = getenv("MM_EPI_BOX")) {  // tuning knob: 32 | 128 rows per TMA store, 0 = st.global
-      const int v = atoi(env);
-      a.c_box = v == 128 ? 128 : (v == 0 ? 0 : 32);
-    }
     if (a.c_tma) {
-      const uint32_t cbox[2] = {32, a.c_box == 128 ? 128u : 32u};
+      const uint32_t cbox[2] = {32, 32};
       st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
                      cbox, "C");
       if (st != MM_OK) return st;

@@ -391,13 +391,11 @@ def test_row_blocks_bit_identical_to_full_product(mm, G):
 
 
 @pytest.mark.parametrize("dt", ["i8", "bf16"])
-@pytest.mark.parametrize("epi", ["32", "128", "0"])
-def test_epilogue_store_modes(mm, dt, epi):
-    """Every C store path of the tcgen05 epilogue — a TMA store per warp chunk (32), one per
-    128-row CTA chunk (128), staged st.global of full lines (0) — on ragged shapes with both
-    tile widths, inside guard bands (bit-exact, nothing written outside C)."""
+def test_epilogue_guard_bands_both_tile_widths(mm, dt):
+    """The eight-warp epilogue (two warps per TMEM lane quarter, one per column half / NT=2
+    region) with TMA stores, on ragged shapes with both tile widths, inside guard bands
+    (bit-exact, nothing written outside C)."""
     out = torch.float32 if dt == "bf16" else torch.int32
-    os.environ["MM_EPI_BOX"] = epi
     try:
         for (m, n, p, nt) in [(300, 200, 520, "1"), (513, 1024, 1100, "2"), (1100, 768, 1700, "2"), (777, 64, 300, "1")]:
             os.environ["MM_NT"] = nt
@@ -412,7 +410,6 @@ def test_epilogue_store_modes(mm, dt, epi):
             assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), (m, n, p, epi)
             assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p, epi)
     finally:
-        os.environ.pop("MM_EPI_BOX", None)
         os.environ.pop("MM_NT", None)
 
 
