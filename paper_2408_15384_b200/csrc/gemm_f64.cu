@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
       uint32_t phase = 0;
       bool ok = true;
       int t, kb0, kb1;
+      pdl_wait();  // programmatic dependent launch: the prologue above overlapped the previous kernel
       for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
         int tm, tn;
         sched.tile_coords(t, tm, tn);
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
       }
+      pdl_launch_dependents();  // all loads issued: the next launch may start its prologue
     }
   } else {
     // ---------------------------------------------------------------- DMMA consumers
@@ -308,8 +310,17 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<pl.sched.nc, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(tmA, tmB, a, pl.sched);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.sched.nc, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = getenv("MM_NO_PDL") ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a, pl.sched);
 }
 
 }  // namespace

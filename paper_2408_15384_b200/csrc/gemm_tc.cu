@@ -185,6 +185,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // l2_hint bit 0: A evict_last; bit 1: B evict_first (else evict_normal)
       const uint64_t pol_a = (args.l2_hint & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
       const uint64_t pol_b = (args.l2_hint & 2) ? l2_policy_evict_first() : l2_policy_evict_normal();
+      // Programmatic dependent launch: everything above (barrier init, TMEM allocation, tensor-map
+      // prefetch) overlapped the previous kernel in the stream; no global memory is touched before
+      // it has completed (the MMA and epilogue only run on data loaded after this wait).
+      pdl_wait();
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         // Wave barrier: start item j only when every CTA has issued all loads of its
         // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (args.wave_sync && j < sched.W) red_release_gpu_add(args.sync, 1u);
       }
+      pdl_launch_dependents();  // all loads issued: the next launch may start its prologue
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (leader CTA)
@@ -590,8 +595,10 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
   attr[0].val.clusterDim.x = CG * MC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // (the occupancy query below: cluster shape only)
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
@@ -606,6 +613,7 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
     attr_set = true;
   }
   *max_clusters = max_cl;
+  cfg.numAttrs = getenv("MM_NO_PDL") ? 1 : 2;  // + programmatic dependent launch (knob: MM_NO_PDL=1 off)
   return cudaSuccess;
 }
 
@@ -613,7 +621,7 @@ template <bool I8, int CG, int NT, int MC>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
                         int num_sms, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int max_cl = 0;
   cudaError_t e = launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl);
   if (e != cudaSuccess) return e;
@@ -626,7 +634,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
 template <bool I8, int CG, int NT, int MC>
 int max_clusters_of(int num_sms) {
   cudaLaunchConfig_t cfg;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int max_cl = 0;
   if (launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl) != cudaSuccess) return 0;
   return max_cl;

@@ -159,6 +159,12 @@ __device__ __forceinline__ void st_cg_d2(void* p, double2 v) {
   asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Wait until the grids this launch depends on have completed and their memory is visible (a no-op
+// when the launch was not programmatic); and let the next launch in the stream begin its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
