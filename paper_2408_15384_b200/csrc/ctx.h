@@ -49,6 +49,21 @@ struct mm_ctx {
 
 namespace mmb {
 
+// Makes the context's device current for the duration of an ABI call (the caller's current
+// device may differ: operands, stream and context belong to ctx->device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 mm_status set_err(mm_ctx* ctx, mm_status s, const char* fmt, ...);
 size_t dtype_in_size(mm_dtype t);
 size_t dtype_out_size(mm_dtype t);

@@ -26,6 +26,8 @@
 // the same four k's for A and B, so each DMMA still adds A[i][k]·B[k][j] over
 // its four k's; only which k's are grouped together changes.
 // Edges: TMA zero-fills out-of-bounds reads; stores are predicated.
+#include <atomic>
+
 #include "kernels.h"
 #include "ptx.cuh"
 #include "sched.cuh"
@@ -304,11 +306,14 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
                         cudaStream_t s) {
   using Cfg = F64Cfg<BM, BN, WM, WN, KS>;
   auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<bool> attr_set[kMaxDevices];  // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!attr_set[dev].load()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev].store(true);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.sched.nc, 1, 1);

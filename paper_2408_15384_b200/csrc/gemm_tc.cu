@@ -23,6 +23,7 @@
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> global).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -586,8 +587,11 @@ template <bool I8, int CG, int NT, int MC>
 cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int num_sms, int* max_clusters) {
   using Cfg = TcCfg<I8, CG, NT, MC>;
   auto kern = gemm_tc_kernel<I8, CG, NT, MC>;
-  static bool attr_set = false;  // per template instance
-  static int max_cl = 0;
+  // per template instance and device (function attributes and occupancy are per device)
+  static std::atomic<int> max_cl_dev[kMaxDevices];  // 0 = not set up yet, -1 = query failed
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   cfg = {};
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
@@ -599,7 +603,8 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;  // (the occupancy query below: cluster shape only)
-  if (!attr_set) {
+  int max_cl = max_cl_dev[dev].load();
+  if (max_cl == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     // all clusters of the persistent grid must be resident together (wave barrier, stream-K waits)
@@ -609,10 +614,10 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
       cudaGetLastError();
       n = 0;
     }
-    max_cl = n;
-    attr_set = true;
+    max_cl = n > 0 ? n : -1;
+    max_cl_dev[dev].store(max_cl);
   }
-  *max_clusters = max_cl;
+  *max_clusters = max_cl > 0 ? max_cl : 0;
   cfg.numAttrs = getenv("MM_NO_PDL") ? 1 : 2;  // + programmatic dependent launch (knob: MM_NO_PDL=1 off)
   return cudaSuccess;
 }

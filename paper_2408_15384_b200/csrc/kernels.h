@@ -9,6 +9,8 @@
 
 namespace mmb {
 
+constexpr int kMaxDevices = 64;  // per-device launch state (function attributes, occupancy)
+
 // Problem as the kernels see it: C (M×N, leading dim ldc elements) = A (M×K) · B (K×N).
 // Paper notation: M = m, K = n, N = p.
 struct GemmArgs {

@@ -418,6 +418,7 @@ void mm_release_comms(mm_ctx* ctx);  // shard.cu
 
 __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   if (!ctx) return;
+  DeviceGuard dg(ctx->device);
   cudaDeviceSynchronize();
   mm_release_comms(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
@@ -437,6 +438,8 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
 __attribute__((visibility("default"))) mm_status mm_gemm(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
                                                          mm_dtype dtype, const void* A, const void* B, void* C,
                                                          void* stream) {
+  if (!ctx) return MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
   if (st != MM_OK) return st;
   return gemm_ld(ctx, m, n, p, dtype, A, n, B, p, C, p, 0, static_cast<cudaStream_t>(stream));
@@ -444,6 +447,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm(mm_ctx* ctx, int64_t m,
 
 __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void* stream) {
   if (!ctx) return MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
   cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "stream sync failed: %s", cudaGetErrorString(e));
   int h = 0;
@@ -467,6 +471,8 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
 __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64_t m, int64_t n, int64_t p,
                                                               mm_dtype dtype, const void* A, const void* B, void* C,
                                                               void* stream) {
+  if (!ctx) return MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
   if (st != MM_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

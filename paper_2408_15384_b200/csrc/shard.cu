@@ -495,6 +495,8 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
                                                                  void* C_local, void* C_full, unsigned flags, int root,
                                                                  void* nccl_comm, void* stream) {
   if (!ctx) return MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
+  if (!ctx) return MM_ERR_USAGE;
   if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32)
     return set_err(ctx, MM_ERR_USAGE, "unknown dtype %d", (int)dtype);
   if (m < 1 || n < 1 || p < 1) return set_err(ctx, MM_ERR_USAGE, "dimensions must be >= 1");
