@@ -448,6 +448,24 @@ def test_int32_accumulate_large_k(mm):
     assert np.all(C[0] == n * 127 * 127) and np.all(C[1] == -n * 127 * 127)
 
 
+@pytest.mark.parametrize("cg", [1, 2])
+def test_int32_overflow_wraps(mm, cg):
+    """Beyond BASELINE.json's range (R10): with n*128^2 > 2^31 - 1
+    the INT32 accumulators wrap modulo 2^32 (measured on the B200: all -128 inputs, n = 131088,
+    exact 2,147,745,792 -> -2,147,221,504), i.e. C equals the oracle's exact int64 sum reduced
+    to int32 two's complement."""
+    m, n, p = 256, 131088, 256
+    os.environ["MM_FORCE_CG"] = str(cg)
+    A = torch.full((m, n), -128, dtype=torch.int8, device="cuda")
+    B = torch.full((n, p), -128, dtype=torch.int8, device="cuda")
+    C = mm.gemm(A, B)
+    mm.sync_check()
+    exact = oracle.gemm_s8(np.full((1, n), -128, np.int8), np.full((n, 1), -128, np.int8))[0, 0]
+    assert exact == n * 128 * 128
+    wrapped = ((int(exact) + 2**31) % 2**32) - 2**31
+    assert torch.all(C == wrapped), np.unique(C.cpu().numpy())
+
+
 def test_host_operand_path(mm):
     """mm_gemm_host (H2D, product, D2H in overlapped row blocks) equals the oracle."""
     for dt in ("f64", "bf16", "i8"):
