@@ -466,6 +466,27 @@ def test_int32_overflow_wraps(mm, cg):
     assert torch.all(C == wrapped), np.unique(C.cpu().numpy())
 
 
+def test_bf16_subnormals_not_flushed(mm):
+    """the configs never produce subnormals, so the hardware's handling is
+    measured here: subnormal bf16 inputs (exponent 0) times 1.0, and normal inputs whose product
+    (2^-70 * 2^-70 = 2^-140) and sums are FP32 subnormals — the tcgen05 BF16 path keeps both
+    exactly (no flush to zero), equal to the oracle's exact double result."""
+    n = 128
+    sub = (np.arange(1, n + 1, dtype=np.uint16) & 0x7F)
+    sub[sub == 0] = 1
+    A = np.zeros((256, n), np.uint16)
+    A[0] = sub
+    A[1, 0], A[1, 1] = 0x1C80, 0x1C80  # 2^-70
+    B = np.zeros((n, 256), np.uint16)
+    B[np.arange(n), np.arange(n)] = 0x3F80  # 1.0 on the diagonal
+    B[0, 200], B[1, 200] = 0x1C80, 0x9C80  # +2^-70, -2^-70 -> row 1 col 200: 2^-140 - 2^-140 = 0
+    B[0, 201] = 0x1C80                      # row 1 col 201: 2^-140
+    Cref, _ = oracle.gemm_bf16(A, B)
+    C = run_gpu(mm, A, B, "bf16")
+    assert np.array_equal(C.astype(np.float64), Cref)
+    assert C[1, 201] == np.float32(2.0 ** -140) and C[0, 5] != 0
+
+
 def test_host_operand_path(mm):
     """mm_gemm_host (H2D, product, D2H in overlapped row blocks) equals the oracle."""
     for dt in ("f64", "bf16", "i8"):
