@@ -42,7 +42,11 @@ constexpr int BBOX_BYTES = BK * 16 * 8;  // 2 KB, box {16 cols, 16 rows}
 // KS: k-block groups of WM x WN consumer warps.  KS = 2 (small tiles): the two groups take the
 // even / odd k-blocks of each tile (twice the DMMA chains in flight per SMSP), and group 1's
 // accumulators are added into group 0's through shared memory before the epilogue.
-template <int BM, int BN, int WM, int WN, int KS = 1>
+// KB: k-blocks per TMA load (small tiles: one 3-D box of A and one of B bring KB consecutive
+// k-blocks into KB consecutive ring slots, so a 32x32 tile's whole K arrives in a few loads — a
+// single thread issuing three 2-D loads per 16-deep k-block was the bottleneck at C1: ~160
+// cycles per load).  B then sits per group as [column box][KB x 16 rows][128 B].
+template <int BM, int BN, int WM, int WN, int KS = 1, int KB = 1>
 struct F64Cfg {
   static constexpr int NTILE = WM * WN;        // warps covering one tile
   static constexpr int NCONS = NTILE * KS;     // consumer warps
@@ -53,8 +57,10 @@ struct F64Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // ~200 KB of operand ring: 6 stages at 128x128, 12 at 64x64, 25 at 32x32 (a whole K <= 384 of a
   // small tile in flight at once: the cold DRAM round trip is paid once, not K/(16*stages) times)
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 64 ? (200 * 1024) / STAGE_BYTES : 64;
-  static constexpr int SCR_BYTES = KS > 1 ? BM * BN * 8 : 0;  // group-1 accumulators
+  static constexpr int STAGES0 = (200 * 1024) / STAGE_BYTES < 64 ? (200 * 1024) / STAGE_BYTES : 64;
+  static constexpr int STAGES = STAGES0 / KB * KB;            // whole groups of KB slots
+  static constexpr int BOX_STRIDE = KB * BBOX_BYTES;          // between B column boxes of one slot
+  static constexpr int SCR_BYTES = (KS - 1) * BM * BN * 8;  // accumulators of groups 1..KS-1
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + 1024;
   static_assert(STAGES >= 4 && 16 * STAGES <= 1024, "ring");
   static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
@@ -64,11 +70,17 @@ struct F64Cfg {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int BM, int BN, int WM, int WN, int KS>
-__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
-    gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args,
+template <int BM, int BN, int WM, int WN, int KS, int KB>
+__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
+    gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3, GemmArgs args,
                     WorkSched sched) {
-  using Cfg = F64Cfg<BM, BN, WM, WN, KS>;
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB>;
+  // optional per-CTA timeline (MM_TRACE=1), globaltimer ns: [0] entry, [1] prologue done, [2] first
+  // load issued, [3] first stage landed (consumer warp 0), [4] first item's k-loop done, [5] first
+  // item stored, [6] exit
+  unsigned long long* tl = args.trace ? args.trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = globaltimer_ns();
   constexpr int NCONS = Cfg::NCONS;
   constexpr int NTILE = Cfg::NTILE;
   constexpr int STAGES = Cfg::STAGES;
@@ -89,15 +101,23 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
   int* err = args.err;
 
   if (warp == NCONS && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    if (KB == 1) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+    } else {
+      tma_prefetch_desc(&tmA3);
+      tma_prefetch_desc(&tmB3);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), NTILE);  // one k-block group consumes each slot
+      // KB == 1: one k-block group of warps consumes each slot; KB > 1: every warp arrives once
+      // per group of KB slots (on its first slot's barrier)
+      mbar_init(empty_bar(s), KB == 1 ? NTILE : NCONS);
     }
     fence_mbar_init();
   }
   __syncthreads();
+  if (tl && threadIdx.x == 0) tl[1] = globaltimer_ns();
 
   if (warp == NCONS) {
     // ---------------------------------------------------------------- TMA producer
@@ -110,17 +130,26 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
       for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
         int tm, tn;
         sched.tile_coords(t, tm, tn);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += KB) {
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) { ok = false; break; }
-          mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+          mbar_arrive_expect_tx(full_bar(stage), KB * Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, full_bar(stage), k0, tm * BM);
+          if constexpr (KB == 1) {
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, full_bar(stage), k0, tm * BM);
 #pragma unroll
-          for (int b = 0; b < Cfg::NBBOX; ++b)
-            tma_load_2d(sB + stage * Cfg::B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), tn * BN + b * 16, k0);
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            for (int b = 0; b < Cfg::NBBOX; ++b)
+              tma_load_2d(sB + stage * Cfg::B_BYTES + b * BBOX_BYTES, &tmB, full_bar(stage), tn * BN + b * 16, k0);
+          } else {
+            // KB k-slabs of A (k-blocks kb..kb+KB-1) and the KB x 16 rows of all column boxes of B
+            tma_load_3d(sA + stage * Cfg::A_BYTES, &tmA3, full_bar(stage), 0, tm * BM, kb);
+            tma_load_3d(sB + stage * Cfg::B_BYTES, &tmB3, full_bar(stage), 0, k0, tn * (BN / 16));
+          }
+          if (tl && j == 0 && kb == kb0) tl[2] = globaltimer_ns();
+          stage += KB;
+          if (stage == STAGES) { stage = 0; phase ^= 1u; }
         }
       }
+      if (tl) tl[7] = globaltimer_ns();  // all loads issued
       pdl_launch_dependents();  // all loads issued: the next launch may start its prologue
     }
   } else {
@@ -144,7 +173,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
     const int a_base0 = (wm * (BM / WM) + arow) * 128 + (kk & 1) * 8;
     const int a_x0 = (kk >> 1) ^ arow;
     // B: column c16 = (ni&1)*4 + bcol in box wn*NI/2 + ni/2; chunk (c16>>1) ^ (k & 7), half c16 & 1.
-    const int b_base0 = wn * (Cfg::NI / 2) * BBOX_BYTES + kk * 128 + (bcol & 1) * 8;
+    const int b_base0 = wn * (Cfg::NI / 2) * Cfg::BOX_STRIDE + kk * 128 + (bcol & 1) * 8;
     const int b_x0 = (bcol >> 1) ^ kk;
     double* C = reinterpret_cast<double*>(args.C);
     double* part = reinterpret_cast<double*>(args.ws);
@@ -162,14 +191,20 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
 #pragma unroll
         for (int ni = 0; ni < Cfg::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-      for (int kb = kb0; kb < kb1; ++kb, ++gk) {
-        if (KS > 1 && (int)(gk % KS) != kgrp) {  // the other group's k-block
+      for (int kb = kb0; kb < kb1; kb += KB) {
+        const int nk = min(KB, kb1 - kb);  // k-blocks in this group (KB == 1: one)
+        if (KB == 1 && KS > 1 && (int)(gk % KS) != kgrp) {  // the other warp group's k-block
+          ++gk;
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
           continue;
         }
         if (!mbar_wait(full_bar(stage), phase, err, 12)) { ok = false; break; }
-        const uint8_t* pa = smem + stage * Cfg::A_BYTES;
-        const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES;
+        if (tl && warp == 0 && lane == 0 && j == 0 && kb == kb0) tl[3] = globaltimer_ns();
+        for (int i = 0; i < nk; ++i) {
+        if (KB > 1 && KS > 1 && (int)((gk + i) % KS) != kgrp) continue;  // the other warp group's k-block
+        // slot (stage + i): A slab at its own slot; B (KB > 1) at the group's B region, k-block i
+        const uint8_t* pa = smem + (stage + i) * Cfg::A_BYTES;
+        const uint8_t* pb = smem + STAGES * Cfg::A_BYTES + stage * Cfg::B_BYTES + i * BBOX_BYTES;
         int a_base, a_x, b_base, b_x;
         asm volatile("mov.b32 %0, %1;" : "=r"(a_base) : "r"(a_base0));
         asm volatile("mov.b32 %0, %1;" : "=r"(a_x) : "r"(a_x0));
@@ -185,7 +220,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
 #pragma unroll
           for (int ni = 0; ni < Cfg::NI; ++ni)
             bf[ni] = *reinterpret_cast<const double*>(
-                pb + b_base + ((((ni & 1) << 1) ^ ((qd & 1) << 2) ^ b_x) << 4) + (ni >> 1) * BBOX_BYTES + qd * 512);
+                pb + b_base + ((((ni & 1) << 1) ^ ((qd & 1) << 2) ^ b_x) << 4) + (ni >> 1) * Cfg::BOX_STRIDE + qd * 512);
           const uint8_t* pa_q = pa + a_base + ((((qd << 1) & 7) ^ a_x) << 4) + ((qd << 1) & 8) * 16;
 #pragma unroll
           for (int mi = 0; mi < Cfg::MI; ++mi) {
@@ -194,6 +229,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
             for (int ni = 0; ni < Cfg::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
           }
         }
+        }  // k-blocks of the group
         // The slot is refilled by TMA (async proxy) once all warps arrived: order this warp's
         // shared-memory fragment loads (generic proxy) before that.  Without the proxy fence
         // ptxas issued the arrive while the last A-fragment load was still in flight, and a
@@ -201,37 +237,49 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_bar(stage));
-        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        gk += nk;
+        stage += KB;
+        if (stage == STAGES) { stage = 0; phase ^= 1u; }
       }
       if (!ok) break;
+      if (tl && warp == 0 && lane == 0 && j == 0) tl[4] = globaltimer_ns();
       if constexpr (KS > 1) {
-        // group 1 hands its partial sums to group 0 through shared memory (fixed order)
-        if (kgrp == 1) {
+        // groups 1..KS-1 hand their partial sums to group 0 through shared memory (added in
+        // group order: fixed, deterministic)
+        if (kgrp >= 1) {
+          double* mine = scr + (size_t)(kgrp - 1) * (BM * BN);
 #pragma unroll
           for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < Cfg::NI; ++ni) {
               const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-              *reinterpret_cast<double2*>(scr + r * BN + cc) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+              *reinterpret_cast<double2*>(mine + r * BN + cc) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
             }
         }
         named_bar(2, NCONS * 32);
         if (kgrp == 0) {
+          for (int g = 1; g < KS; ++g) {
+            const double* other = scr + (size_t)(g - 1) * (BM * BN);
 #pragma unroll
-          for (int mi = 0; mi < Cfg::MI; ++mi)
+            for (int mi = 0; mi < Cfg::MI; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < Cfg::NI; ++ni) {
-              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-              const double2 v = *reinterpret_cast<const double2*>(scr + r * BN + cc);
-              acc[mi][ni][0] += v.x;
-              acc[mi][ni][1] += v.y;
-            }
+              for (int ni = 0; ni < Cfg::NI; ++ni) {
+                const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+                const double2 v = *reinterpret_cast<const double2*>(other + r * BN + cc);
+                acc[mi][ni][0] += v.x;
+                acc[mi][ni][1] += v.y;
+              }
+          }
         }
         named_bar(3, NCONS * 32);
         if (kgrp != 0) continue;  // group 0 finishes the tile
       }
 
       const bool whole = (kb0 == 0 && kb1 == num_kb);
+      struct StoreMark {  // first item's results written (any path)
+        unsigned long long* tl; bool on;
+        __device__ ~StoreMark() { if (on) tl[5] = globaltimer_ns(); }
+      } mark{tl, tl != nullptr && warp == 0 && lane == 0 && j == 0};
       if (!whole && kb0 != 0) {
         // ---- contributor: publish the partial tile, then signal the finisher
         double* slot = part + (size_t)c * (BM * BN);
@@ -299,13 +347,14 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS>::THREADS, 1)
   }
   __syncwarp();
   __syncthreads();
+  if (tl && threadIdx.x == 0) tl[6] = globaltimer_ns();
 }
 
-template <int BM, int BN, int WM, int WN, int KS>
-cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
-                        cudaStream_t s) {
-  using Cfg = F64Cfg<BM, BN, WM, WN, KS>;
-  auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS>;
+template <int BM, int BN, int WM, int WN, int KS, int KB = 1>
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3, const CUtensorMap& tmB3,
+                        const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS, KB>;
   static std::atomic<bool> attr_set[kMaxDevices];  // function attributes are per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -325,7 +374,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = getenv("MM_NO_PDL") ? 0 : 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a, pl.sched);
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA3, tmB3, a, pl.sched);
 }
 
 }  // namespace
@@ -360,7 +409,13 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   if (const char* e = getenv("MM_F64_STREAMK")) mode = atoi(e) != 0 ? 1 : 0;  // tuning knob
   // small tiles: two k-block groups of warps per CTA (latency-bound DMMA chains)
   pl.ks = pl.bm == 32 ? 2 : 1;
-  if (const char* e = getenv("MM_F64_KS")) pl.ks = (pl.bm == 32 && atoi(e) == 2) ? 2 : 1;  // tuning knob
+  if (const char* e = getenv("MM_F64_KS")) {  // tuning knob: 1 | 2 | 4 (32x32 tiles only)
+    const int v = atoi(e);
+    pl.ks = (pl.bm == 32 && (v == 2 || v == 4 || v == 8 || v == 44)) ? v : 1;
+  }
+  // 32x32 whole tiles: 4 k-blocks per TMA load (the caller drops to 1 unless n, p are 16-multiples)
+  pl.kb = (pl.bm == 32 && mode == 0 && (pl.ks == 1 || pl.ks == 2)) ? 4 : 1;
+  if (const char* e = getenv("MM_F64_KB")) pl.kb = (pl.kb == 4 && atoi(e) == 4) ? 4 : 1;  // tuning knob
   pl.sched = sched_build(tiles_m, tiles_n, 8, num_kb, (int)std::max<int64_t>(1, nc), mode);
   pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
   pl.flag_count = (int)T;
@@ -374,12 +429,19 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
   b_box[1] = BK;
 }
 
-cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
-                            cudaStream_t s) {
-  if (pl.bm == 128) return launch_impl<128, 128, 2, 4, 1>(tmA, tmB, a, pl, s);
-  if (pl.bm == 64) return launch_impl<64, 64, 2, 4, 1>(tmA, tmB, a, pl, s);
-  if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2>(tmA, tmB, a, pl, s);
-  return launch_impl<32, 32, 2, 2, 1>(tmA, tmB, a, pl, s);
+cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
+                            const CUtensorMap& tmB3, const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
+  if (pl.bm == 128) return launch_impl<128, 128, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  if (pl.bm == 64) return launch_impl<64, 64, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  if (pl.kb > 1) {  // 32x32, grouped loads (KB = 4 k-blocks per TMA load)
+    if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);
+    return launch_impl<32, 32, 2, 2, 1, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  }
+  if (pl.ks == 8) return launch_impl<32, 32, 1, 1, 8>(tmA, tmB, tmA3, tmB3, a, pl, s);   // 8 warps, each 32x32 over 1/8 of K
+  if (pl.ks == 44) return launch_impl<32, 32, 2, 2, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);  // 16 warps, 16x16 over 1/4 of K
+  if (pl.ks == 4) return launch_impl<32, 32, 1, 1, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);   // 4 warps, each 32x32 over 1/4 of K
+  if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  return launch_impl<32, 32, 2, 2, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
 }
 
 }  // namespace mmb

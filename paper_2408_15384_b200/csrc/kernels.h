@@ -32,7 +32,8 @@ struct GemmArgs {
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).
 struct F64Plan {
   int bm, bn;       // CTA tile
-  int ks;           // k-block groups of consumer warps (2: small tiles)
+  int ks;           // k-block groups of consumer warps (small tiles)
+  int kb;           // k-blocks per TMA load (small tiles: 3-D slab maps; 1 = 2-D boxes)
   WorkSched sched;  // whole-tile waves + split tail over sched.nc persistent CTAs
   size_t ws_bytes;
   int flag_count;
@@ -54,8 +55,10 @@ void tc_box_dims(bool i8, int cg, int mc, uint32_t* a_box /*[2]*/, uint32_t* b_b
 int max_clusters(bool i8, int cg, int nt, int mc, int num_sms);
 
 // FP64 on DMMA (mma.sync m8n8k4) with TMA-fed smem ring.
-cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, const F64Plan& pl,
-                            cudaStream_t s);
+// tmA3 / tmB3: the 3-D slab maps used when pl.kb > 1 (A {16, m, n/16} box {16, bm, kb};
+// B {16, n, p/16} box {16, 16 kb, bn/16}); pass tmA / tmB otherwise.
+cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
+                            const CUtensorMap& tmB3, const GemmArgs& a, const F64Plan& pl, cudaStream_t s);
 void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box);
 
 // Copy a rows×cols matrix (pitch src_ld elements) into dst (pitch dst_ld >= cols), zero-filling

@@ -92,6 +92,25 @@ mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_
   return MM_OK;
 }
 
+// Row-major rows x cols matrix (pitch ld elements) seen as 3-D {16, rows, cols/16}: element
+// (r, 16*o + i) at dims (i, r, o) — one box covers several consecutive 16-column slabs (cols % 16 == 0).
+mm_status encode_3d_slabs(mm_ctx* ctx, CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                          const uint32_t box[3], const char* what) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_err(ctx, MM_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[3] = {16, (cuuint64_t)rows, (cuuint64_t)(cols / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128};
+  cuuint32_t boxd[3] = {box[0], box[1], box[2]};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(ptr), dims, strides, boxd, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA 3-D encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
+                   (long long)rows, (long long)cols, (long long)ld, (int)r);
+  return MM_OK;
+}
+
 inline bool tma_ok(const void* p, int64_t ld, size_t esz) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * (int64_t)esz) % 16 == 0);
 }
@@ -208,7 +227,8 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     return MM_OK;
   };
   if (dtype == MM_F64) {
-    const F64Plan pl = f64_plan(m, p, n, ctx->num_sms);
+    F64Plan pl = f64_plan(m, p, n, ctx->num_sms);
+    if (pl.kb > 1 && (n % 16 != 0 || p % 16 != 0)) pl.kb = 1;  // grouped loads need exact 16-slabs
     mm_status st = ensure_sk(pl.ws_bytes, (size_t)pl.flag_count);
     if (st != MM_OK) return st;
     f64_box_dims(pl, abox, bbox);
@@ -216,7 +236,43 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (st != MM_OK) return st;
     st = encode_2d(ctx, &tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
-    e = launch_gemm_f64(tmA, tmB, a, pl, s);
+    const bool ftrace = getenv("MM_TRACE") != nullptr;
+    if (ftrace) {
+      if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
+        return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
+      cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 8 * sizeof(unsigned long long), s);
+      a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
+    }
+    // small tiles: several k-blocks per TMA load (3-D slab maps), when K and p are 16-multiples
+    CUtensorMap tmA3 = tmA, tmB3 = tmB;
+    if (pl.kb > 1) {
+      const uint32_t a3[3] = {16, (uint32_t)pl.bm, (uint32_t)pl.kb};
+      const uint32_t b3[3] = {16, (uint32_t)(16 * pl.kb), (uint32_t)(pl.bn / 16)};
+      st = encode_3d_slabs(ctx, &tmA3, Ause, m, n, padA ? ldA2 : lda, a3, "A (k-slab groups)");
+      if (st != MM_OK) return st;
+      st = encode_3d_slabs(ctx, &tmB3, Buse, n, p, padB ? ldB2 : ldb, b3, "B (column-slab groups)");
+      if (st != MM_OK) return st;
+    }
+    e = launch_gemm_f64(tmA, tmB, tmA3, tmB3, a, pl, s);
+    if (e == cudaSuccess && ftrace) {
+      std::vector<unsigned long long> h(4096 * 8);
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h.data(), ctx->trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      unsigned long long e0 = ~0ull;
+      for (int c = 0; c < pl.sched.nc; ++c) if (h[(size_t)c * 8]) e0 = std::min(e0, h[(size_t)c * 8]);
+      double acc[8] = {0};
+      int cnt[8] = {0};
+      for (int c = 0; c < pl.sched.nc; ++c)
+        for (int k = 0; k < 8; ++k)
+          if (h[(size_t)c * 8 + k]) { acc[k] += (double)(h[(size_t)c * 8 + k] - e0); ++cnt[k]; }
+      fprintf(stderr, "[mm trace f64] m=%lld n=%lld p=%lld tile %d ks %d CTAs %d | us after first entry (CTA avg): entry %.2f "
+              "prologue %.2f first-load %.2f first-data %.2f k-loop-done %.2f stored %.2f exit %.2f | loads issued %.2f\n",
+              (long long)m, (long long)n, (long long)p, pl.bm, pl.ks, pl.sched.nc,
+              cnt[0] ? 1e-3 * acc[0] / cnt[0] : 0.0, cnt[1] ? 1e-3 * acc[1] / cnt[1] : 0.0,
+              cnt[2] ? 1e-3 * acc[2] / cnt[2] : 0.0, cnt[3] ? 1e-3 * acc[3] / cnt[3] : 0.0,
+              cnt[4] ? 1e-3 * acc[4] / cnt[4] : 0.0, cnt[5] ? 1e-3 * acc[5] / cnt[5] : 0.0,
+              cnt[6] ? 1e-3 * acc[6] / cnt[6] : 0.0, cnt[7] ? 1e-3 * acc[7] / cnt[7] : 0.0);
+    }
   } else {
     if (beta_one) return set_err(ctx, MM_ERR_UNSUPPORTED, "accumulate (beta=1) is only implemented for MM_F64");
     const bool i8 = dtype == MM_S8_S32;

@@ -221,18 +221,22 @@ def test_split_tile_fixup_repeated(mm, dt):
             os.environ.pop(k, None)
 
 
-@pytest.mark.parametrize("tile", ["32", "32ks1", "64", "128"])
+@pytest.mark.parametrize("tile", ["32ks4", "32ks2", "32ks1", "64", "128"])
 @pytest.mark.parametrize("streamk", ["0", "1"])
 def test_f64_tiles_and_schedules(mm, tile, streamk):
-    """FP64 kernel at every CTA tile (32x32 with two k-block groups of 4 warps or one; 64x64 /
+    """FP64 kernel at every CTA tile (32x32 with 4 k-block groups of one warp, 2 of 4 warps, or one
+    group of 4; 64x64 /
     128x128 with 8 warps), with whole-tile waves only or with the split last wave, on ragged
     and multi-wave shapes; the exact-integer inputs make every tile, seam, k-group and
     partial-tile sum bit-exact."""
     os.environ["MM_F64_TILE"] = tile[:2] if tile.startswith("32") else tile
-    os.environ["MM_F64_KS"] = "1" if tile == "32ks1" else "2"
+    os.environ["MM_F64_KS"] = tile[4:] if tile.startswith("32") else "1"
     os.environ["MM_F64_STREAMK"] = streamk
     try:
-        for (m, n, p) in [(256, 256, 256), (300, 200, 520), (129, 1000, 77), (1100, 768, 1700), (2100, 300, 2050)]:
+        for (m, n, p) in [(256, 256, 256), (300, 200, 520), (129, 1000, 77), (1100, 768, 1700), (2100, 300, 2050),
+                          (300, 208, 528), (100, 1024, 160), (33, 16, 48), (250, 80, 240)]:
+            # (16-multiple n and p: the 32x32 whole-tile path loads 4 k-blocks per 3-D TMA box,
+            # incl. a partial last group when n/16 is not a multiple of 4)
             A, B = gen("f64", "exact", 47, m, n, p, 2049)
             Cref, D = ref("f64", A, B)
             check("f64", run_gpu(mm, A, B, "f64"), Cref, D, exact=True)
