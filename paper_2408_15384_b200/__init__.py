@@ -67,6 +67,7 @@ class Context:
 
 
 _local = threading.local()
+_MM_GEMM = None  # mm_gemm, resolved on first use
 
 
 def context(device: int | None = None) -> Context:
@@ -101,20 +102,33 @@ def _check_operands(A: torch.Tensor, B: torch.Tensor):
     return A.shape[0], A.shape[1], B.shape[1], IN_DTYPE[A.dtype]
 
 
+try:  # the raw current-stream handle without constructing a torch.cuda.Stream (~2 us per call)
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover
+    def _raw_stream(idx):
+        return torch.cuda.current_stream(idx).cuda_stream
+
+
 def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
          stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """C = A·B on the GPU (async on `stream`, default: torch's current stream)."""
     m, n, p, dt = _check_operands(A, B)
-    if not A.is_cuda or A.device != B.device:
+    dev = A.device
+    if dev.type != "cuda" or B.device != dev:
         raise ValueError("gemm expects A and B on the same CUDA device (use gemm_host for host operands)")
     if out is None:
-        out = torch.empty((m, p), dtype=OUT_DTYPE[dt], device=A.device)
-    elif out.shape != (m, p) or out.dtype != OUT_DTYPE[dt] or not out.is_contiguous() or out.device != A.device:
-        raise ValueError(f"out must be a contiguous {OUT_DTYPE[dt]} ({m}, {p}) tensor on {A.device}")
-    ctx = context(A.device.index)
-    s = stream if stream is not None else torch.cuda.current_stream(A.device)
-    ctx.check(_lib.load().mm_gemm(ctx.handle, m, n, p, dt, A.data_ptr(), B.data_ptr(), out.data_ptr(),
-                                  s.cuda_stream))
+        out = torch.empty((m, p), dtype=OUT_DTYPE[dt], device=dev)
+    elif out.shape != (m, p) or out.dtype != OUT_DTYPE[dt] or not out.is_contiguous() or out.device != dev:
+        raise ValueError(f"out must be a contiguous {OUT_DTYPE[dt]} ({m}, {p}) tensor on {dev}")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    ctx = context(idx)
+    sh = stream.cuda_stream if stream is not None else _raw_stream(idx)
+    global _MM_GEMM
+    if _MM_GEMM is None:
+        _MM_GEMM = _lib.load().mm_gemm
+    st = _MM_GEMM(ctx.handle, m, n, p, dt, A.data_ptr(), B.data_ptr(), out.data_ptr(), sh)
+    if st:
+        ctx.check(st)
     return out
 
 

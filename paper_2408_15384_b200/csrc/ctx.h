@@ -44,6 +44,14 @@ struct mm_ctx {
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   uint64_t launches = 0;  // kernels launched by this context
+  // encoded tensor maps of recent calls (host cost of cuTensorMapEncodeTiled per call), keyed by
+  // everything the encoding depends on; round-robin replacement
+  struct MapEntry {
+    uint64_t key[8];
+    CUtensorMap map;
+  };
+  MapEntry map_cache[32] = {};
+  int map_cache_used = 0, map_cache_next = 0;
   std::string last_error;
 };
 

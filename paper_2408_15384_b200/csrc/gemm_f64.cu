@@ -29,6 +29,7 @@
 #include <atomic>
 
 #include "kernels.h"
+#include "knobs.h"
 #include "ptx.cuh"
 #include "sched.cuh"
 
@@ -373,7 +374,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = getenv("MM_NO_PDL") ? 0 : 1;
+  cfg.numAttrs = knob("MM_NO_PDL") ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA3, tmB3, a, pl.sched);
 }
 
@@ -386,7 +387,7 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   // CTA one whole tile, no fix-up: C1 = 64 tiles); else 64x64 (measured: 512^3 20.5 us at 64x64
   // split vs 26.6 us at 32x32 split, tools/ab_gpu.py).
   pl.bm = pl.bn = tiles(128) >= num_sms ? 128 : (tiles(32) <= num_sms ? 32 : 64);
-  if (const char* e = getenv("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 128
+  if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 128
     const int v = atoi(e);
     if (v == 32 || v == 64 || v == 128) pl.bm = pl.bn = v;
   }
@@ -406,16 +407,16 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
     nc = std::min<int64_t>(nc, std::max<int64_t>(1, T * num_kb / 4));
     mode = 1;
   }
-  if (const char* e = getenv("MM_F64_STREAMK")) mode = atoi(e) != 0 ? 1 : 0;  // tuning knob
+  if (const char* e = knob("MM_F64_STREAMK")) mode = atoi(e) != 0 ? 1 : 0;  // tuning knob
   // small tiles: two k-block groups of warps per CTA (latency-bound DMMA chains)
   pl.ks = pl.bm == 32 ? 2 : 1;
-  if (const char* e = getenv("MM_F64_KS")) {  // tuning knob: 1 | 2 | 4 (32x32 tiles only)
+  if (const char* e = knob("MM_F64_KS")) {  // tuning knob: 1 | 2 | 4 (32x32 tiles only)
     const int v = atoi(e);
     pl.ks = (pl.bm == 32 && (v == 2 || v == 4 || v == 8 || v == 44)) ? v : 1;
   }
   // 32x32 whole tiles: 4 k-blocks per TMA load (the caller drops to 1 unless n, p are 16-multiples)
   pl.kb = (pl.bm == 32 && mode == 0 && (pl.ks == 1 || pl.ks == 2)) ? 4 : 1;
-  if (const char* e = getenv("MM_F64_KB")) pl.kb = (pl.kb == 4 && atoi(e) == 4) ? 4 : 1;  // tuning knob
+  if (const char* e = knob("MM_F64_KB")) pl.kb = (pl.kb == 4 && atoi(e) == 4) ? 4 : 1;  // tuning knob
   pl.sched = sched_build(tiles_m, tiles_n, 8, num_kb, (int)std::max<int64_t>(1, nc), mode);
   pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
   pl.flag_count = (int)T;

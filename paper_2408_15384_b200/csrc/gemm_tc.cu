@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "kernels.h"
+#include "knobs.h"
 #include "ptx.cuh"
 #include "sched.cuh"
 
@@ -561,7 +562,7 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // measured best (tools/sweep_raster.py): 256-wide tiles 8 tile-rows x ~9 tile-cols per 74-cluster wave;
   // 512-wide tiles 16 x ~4.6
   int group_m = (nt == 2 ? 16 : 8) / mc;
-  if (const char* e = getenv("MM_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
+  if (const char* e = knob("MM_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
   const int num_kb = (int)((K + bk - 1) / bk);
   const int64_t T = (int64_t)tiles_m * tiles_n;
   int64_t nc = num_sms / (cg * mc);
@@ -577,7 +578,7 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
   // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
   int mode = (!i8 && tail > 0 && nt == 1 && mc == 1 && 2 * tail <= nc && num_kb >= 8) ? 2 : 0;
-  if (const char* e = getenv("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
+  if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
   if (mode == 2 && (nt != 1 || 2 * tail > nc)) mode = 1;  // landing: 256-wide tiles, one partner per tile
   return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)nc, mode);
@@ -618,7 +619,7 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
     max_cl_dev[dev].store(max_cl);
   }
   *max_clusters = max_cl > 0 ? max_cl : 0;
-  cfg.numAttrs = getenv("MM_NO_PDL") ? 1 : 2;  // + programmatic dependent launch (knob: MM_NO_PDL=1 off)
+  cfg.numAttrs = knob("MM_NO_PDL") ? 1 : 2;  // + programmatic dependent launch (knob: MM_NO_PDL=1 off)
   return cudaSuccess;
 }
 

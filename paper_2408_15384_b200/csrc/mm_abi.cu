@@ -13,6 +13,7 @@
 
 #include "ctx.h"
 #include "kernels.h"
+#include "knobs.h"
 
 #define MM_VERSION "0.1.0"
 
@@ -74,9 +75,28 @@ EncodeTiledFn get_encode() {
   return g_encode;
 }
 
+// Tensor-map cache lookup / insert (ctx->map_cache).
+bool map_cache_get(mm_ctx* ctx, const uint64_t (&key)[8], CUtensorMap* out) {
+  for (int i = 0; i < ctx->map_cache_used; ++i)
+    if (memcmp(ctx->map_cache[i].key, key, sizeof key) == 0) {
+      *out = ctx->map_cache[i].map;
+      return true;
+    }
+  return false;
+}
+void map_cache_put(mm_ctx* ctx, const uint64_t (&key)[8], const CUtensorMap& m) {
+  const int n = sizeof(ctx->map_cache) / sizeof(ctx->map_cache[0]);
+  const int i = ctx->map_cache_used < n ? ctx->map_cache_used++ : (ctx->map_cache_next++ % n);
+  memcpy(ctx->map_cache[i].key, key, sizeof key);
+  ctx->map_cache[i].map = m;
+}
+
 // Row-major rows×cols matrix with pitch `ld` elements → 2-D tensor map {cols, rows}.
 mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_t esz, const void* ptr, int64_t rows,
                     int64_t cols, int64_t ld, const uint32_t box[2], const char* what) {
+  const uint64_t key[8] = {2, (uint64_t)(uintptr_t)ptr, (uint64_t)rows, (uint64_t)cols, (uint64_t)ld,
+                           ((uint64_t)box[0] << 32) | box[1], ((uint64_t)dt << 32) | (uint64_t)esz, 128};
+  if (map_cache_get(ctx, key, map)) return MM_OK;
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_err(ctx, MM_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable from the driver");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -89,6 +109,7 @@ mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_
   if (r != CUDA_SUCCESS)
     return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
                    (long long)rows, (long long)cols, (long long)ld, (int)r);
+  map_cache_put(ctx, key, *map);
   return MM_OK;
 }
 
@@ -96,6 +117,9 @@ mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_
 // (r, 16*o + i) at dims (i, r, o) — one box covers several consecutive 16-column slabs (cols % 16 == 0).
 mm_status encode_3d_slabs(mm_ctx* ctx, CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
                           const uint32_t box[3], const char* what) {
+  const uint64_t key[8] = {3, (uint64_t)(uintptr_t)ptr, (uint64_t)rows, (uint64_t)cols, (uint64_t)ld,
+                           ((uint64_t)box[0] << 32) | box[1], (uint64_t)box[2], 0};
+  if (map_cache_get(ctx, key, map)) return MM_OK;
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_err(ctx, MM_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable from the driver");
   cuuint64_t dims[3] = {16, (cuuint64_t)rows, (cuuint64_t)(cols / 16)};
@@ -108,6 +132,7 @@ mm_status encode_3d_slabs(mm_ctx* ctx, CUtensorMap* map, const void* ptr, int64_
   if (r != CUDA_SUCCESS)
     return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA 3-D encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
                    (long long)rows, (long long)cols, (long long)ld, (int)r);
+  map_cache_put(ctx, key, *map);
   return MM_OK;
 }
 
@@ -122,7 +147,7 @@ bool ranges_overlap(const void* a, size_t abytes, const void* b, size_t bbytes) 
 }
 
 int force_cg() {
-  const char* e = getenv("MM_FORCE_CG");
+  const char* e = knob("MM_FORCE_CG");
   if (!e) return 0;
   int v = atoi(e);
   return (v == 1 || v == 2) ? v : 0;
@@ -180,7 +205,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   // then the tiles of a wave must walk K together to share A/B slabs.
   const double operand_bytes = (double)(m * n + n * p) * (double)esz;
   int wave_sync = ctx->wave_sync;
-  if (const char* e = getenv("MM_WAVE_SYNC")) wave_sync = atoi(e);  // tuning knob (0 off, 1 auto, 2 on)
+  if (const char* e = knob("MM_WAVE_SYNC")) wave_sync = atoi(e);  // tuning knob (0 off, 1 auto, 2 on)
   a.wave_sync = wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (wave_sync > 1);
 
   CUtensorMap tmA, tmB;
@@ -194,8 +219,8 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.l2_hint = 0;
   a.trace = nullptr;
   a.debug = 0;
-  if (const char* env = getenv("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
-  const bool trace = getenv("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
+  if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
+  const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
     if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
@@ -203,7 +228,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     cudaMemsetAsync(ctx->trace_buf, 0, 4096 * 48 * sizeof(unsigned long long), s);
     a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
   }
-  if (const char* env = getenv("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
+  if (const char* env = knob("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
   // stream-K workspace (partial tiles) + self-resetting per-tile counters, shared by both kernels
   auto ensure_sk = [&](size_t ws_bytes, size_t flag_count) -> mm_status {
     if (ctx->sk_flag_count < flag_count) {
@@ -236,7 +261,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (st != MM_OK) return st;
     st = encode_2d(ctx, &tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
-    const bool ftrace = getenv("MM_TRACE") != nullptr;
+    const bool ftrace = knob("MM_TRACE") != nullptr;
     if (ftrace) {
       if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
         return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
@@ -286,10 +311,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     // 16384, 3.46 waves of 512-wide tiles vs 6.92 of 256-wide ones) runs 6 % faster at NT=2.
     const int64_t tiles_nt2 = ((m + 255) / 256) * ((p + 511) / 512);
     int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= ctx->num_sms / 2)) ? 2 : 1;
-    if (const char* env = getenv("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // two CTA pairs per cluster sharing (multicasting) every B slab
     int mc = 1;
-    if (const char* env = getenv("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    if (const char* env = knob("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     size_t ws_bytes = 0, flag_count = 0;
     tc_plan_needs(i8, cg, nt, mc, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
     mm_status st = ensure_sk(ws_bytes, flag_count);
@@ -304,7 +329,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     CUtensorMap tmC;
     memset(&tmC, 0, sizeof tmC);
     a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
-    if (const char* env = getenv("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
+    if (const char* env = knob("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
     if (a.c_tma) {
       const uint32_t cbox[2] = {32, 32};
       st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
@@ -456,7 +481,8 @@ __attribute__((visibility("default"))) mm_status mm_create(int device, void* wor
   ctx->cc_minor = prop.minor;
   ctx->user_ws = workspace;
   ctx->user_ws_bytes = workspace ? workspace_bytes : 0;
-  if (const char* e = getenv("MM_WAVE_SYNC")) ctx->wave_sync = atoi(e);
+  knobs_refresh();
+  if (const char* e = knob("MM_WAVE_SYNC")) ctx->wave_sync = atoi(e);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -495,6 +521,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm(mm_ctx* ctx, int64_t m,
                                                          mm_dtype dtype, const void* A, const void* B, void* C,
                                                          void* stream) {
   if (!ctx) return MM_ERR_USAGE;
+  knobs_refresh();
   DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
   if (st != MM_OK) return st;
@@ -528,6 +555,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64
                                                               mm_dtype dtype, const void* A, const void* B, void* C,
                                                               void* stream) {
   if (!ctx) return MM_ERR_USAGE;
+  knobs_refresh();
   DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
   if (st != MM_OK) return st;
@@ -552,13 +580,13 @@ __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64
   const int64_t small = (int64_t)64 << 20;
   const bool tiny = (double)(m * n + n * p) * ei < (double)small;
   int64_t nblk = 4;  // measured best for C4 (tools/e2e_probe.py: 28.6 ms vs 31.5 ms at 8)
-  if (const char* env = getenv("MM_HOST_BLOCKS")) nblk = std::max<int64_t>(1, atoll(env));  // tuning knob
+  if (const char* env = knob("MM_HOST_BLOCKS")) nblk = std::max<int64_t>(1, atoll(env));  // tuning knob
   const int64_t rb = tiny ? m : std::min(m, round_up((m + nblk - 1) / nblk, 256));
   const int64_t cb = tiny ? p : std::min(p, round_up((p + nblk - 1) / nblk, 256));
   const int I = (int)((m + rb - 1) / rb), J = (int)((p + cb - 1) / cb);
   std::vector<cudaEvent_t> evA(I), evB(J), evC((size_t)I * J);
   cudaEvent_t evStart;
-  const bool trace = getenv("MM_HOST_TRACE") != nullptr;  // debug: print the copy/compute timeline
+  const bool trace = knob("MM_HOST_TRACE") != nullptr;  // debug: print the copy/compute timeline
   const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
   std::vector<cudaEvent_t> evD((size_t)I * J);
   cudaEventCreateWithFlags(&evStart, evflags);

@@ -33,6 +33,7 @@
 
 #include "ctx.h"
 #include "kernels.h"
+#include "knobs.h"
 
 namespace mmb {
 namespace {
@@ -258,7 +259,7 @@ static mm_status row_block(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtyp
     // B broadcast in column panels, double-buffered on a communication stream, so the
     // broadcast of panel j+1 overlaps the product C[:, panel j] = A · B[:, panel j].
     int64_t npan = 8;
-    if (const char* e = getenv("MM_BCAST_PANELS")) npan = std::max<int64_t>(1, atoll(e));  // tuning knob
+    if (const char* e = knob("MM_BCAST_PANELS")) npan = std::max<int64_t>(1, atoll(e));  // tuning knob
     int64_t w = (p + npan - 1) / npan;
     w = (w + 15) / 16 * 16;  // 16-element multiple: every panel pitch is 16-B aligned for TMA
     if (w > p) w = p;
@@ -400,7 +401,7 @@ static mm_status summa_2d(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
     NCCL_CHECK(ctx, api.GroupEnd());
   }
   int64_t panel = 2048;
-  if (const char* e = getenv("MM_SUMMA_PANEL")) panel = std::max<int64_t>(16, atoll(e));
+  if (const char* e = knob("MM_SUMMA_PANEL")) panel = std::max<int64_t>(16, atoll(e));
   const int np = mm_summa_panels(n, pr, pc, panel, 0, nullptr, nullptr, nullptr, nullptr);
   std::vector<int64_t> k0(np), kw(np);
   std::vector<int> ao(np), bo(np);
@@ -495,6 +496,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
                                                                  void* C_local, void* C_full, unsigned flags, int root,
                                                                  void* nccl_comm, void* stream) {
   if (!ctx) return MM_ERR_USAGE;
+  knobs_refresh();
   DeviceGuard dg(ctx->device);
   if (!ctx) return MM_ERR_USAGE;
   if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32)
