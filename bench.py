@@ -342,6 +342,30 @@ def main():
     launches = mm.launches() - launches0 - args.warmup * (1 if rows > 0 else 0)
     value = flops_total / (ms * 1e-3) / 1e12
 
+    # ---- context: cuBLAS on the same operands and the same bf16 -> fp32 product (torch.mm out_dtype),
+    # back-to-back like the timed steps above (sustained regime); not part of the result
+    library = None
+    if rank == 0 and rows > 0 and not args.no_per_config:
+        try:
+            C_lib = torch.empty(rows, P, dtype=torch.float32, device="cuda")
+            lib_step = lambda: torch.mm(A, B, out_dtype=torch.float32, out=C_lib)  # noqa: E731
+            k = max(10, args.steps // 5)
+            lib_ms, ours_ms = [], []
+            for _ in range(3):  # alternating windows: the same thermal / power state for both
+                lib_ms.append(device_time_steps(lib_step, k, 2))
+                ours_ms.append(device_time_steps(step, k, 2))
+            fl = 2.0 * rows * N_ * P
+            ml, mo = statistics.median(lib_ms), statistics.median(ours_ms)
+            library = {"name": "cuBLAS via torch.mm(A, B, out_dtype=float32), same operands and product",
+                       "ms_per_step": round(ml, 4), "tflops": round(fl / (ml * 1e-3) / 1e12, 1),
+                       "ours_ms_per_step_same_windows": round(mo, 4),
+                       "ours_tflops_same_windows": round(fl / (mo * 1e-3) / 1e12, 1),
+                       "ours_over_cublas": round(ml / mo, 4),
+                       "how": f"3 alternating windows of {k} back-to-back steps each, medians"}
+            del C_lib
+        except Exception as e:  # noqa: BLE001
+            library = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+
     # ---- roofline of the dominant kernel (the tcgen05 BF16 kernel is the whole step)
     per_rank_flops = 2.0 * rows * N_ * P
     achieved = per_rank_flops / (ms * 1e-3) / 1e12 if rows else 0.0
@@ -461,7 +485,8 @@ def main():
                        "parallelism": f"row-block x{world} (B resident on every rank)" if world > 1 else "single GPU",
                        "l2": "operands larger than L2 (A+B 1 GiB, C 1 GiB vs 126 MB): no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "with_comm": with_comm, "per_config": per_config, "protocol": protocol,
+            "clocks": clocks, "with_comm": with_comm, "library_baseline": library, "per_config": per_config,
+            "protocol": protocol,
             "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
                                        "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
                                        "vs_spec_2250": round(value / world / 2250.0, 4)},
