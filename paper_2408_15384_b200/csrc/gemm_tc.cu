@@ -266,7 +266,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (leader CTA)
-    if (rank == 0 && lane == 0) {
+    // The whole warp runs the loop (barrier waits, descriptor arithmetic: warp-uniform, so the
+    // compiler keeps them in uniform registers); lane 0 alone issues the MMAs and commits.
+    // Issuing from a divergent single-lane branch made every tcgen05.mma a waterfall of
+    // ELECT / R2UR.BROADCAST / BRA.U.ANY around its operands.
+    if (rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       bool ok = true;
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
             const uint64_t bdesc =
                 umma_desc_sw128(sb + rr * Cfg::REGION_BYTES + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-            tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (!first_kb || kk != 0) ? 1u : 0u);
+            if (lane == 0) tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (!first_kb || kk != 0) ? 1u : 0u);
           }
         }
       };
@@ -294,14 +298,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool r = CG == 2 ? mbar_wait_cluster(tempty_bar(a), parity, err, 2) : mbar_wait(tempty_bar(a), parity, err, 2);
         if (args.trace) tr_tempty += globaltimer_ns() - tt0;
         tc_fence_after();
-        return r;
+        return __all_sync(0xffffffffu, r) != 0;
       };
       auto wait_full = [&](int stg, uint32_t ph) {
         const uint64_t tf0 = args.trace ? globaltimer_ns() : 0;
         const bool r = mbar_wait(full_bar(stg), ph, err, 3);
         if (args.trace) tr_full += globaltimer_ns() - tf0;
         tc_fence_after();
-        return r;
+        return __all_sync(0xffffffffu, r) != 0;
       };
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         const int acc = j % Cfg::NBUF;
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t p0 = phase;
           for (int i = 0; i < pre; ++i) {
             if (!wait_full(stage, phase)) { ok = false; break; }
-            if (tl && i == 0 && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
+            if (tl && lane == 0 && i == 0 && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
             issue(d_tmem, stage, i == 0, 0, 1);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
           }
@@ -329,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase = p0;
           for (int i = 0; i < pre; ++i) {
             issue(d_tmem, stage, i == 0, 1, 2);
-            tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+            if (lane == 0) tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+            __syncwarp();
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
           }
           kb = kb0 + pre;
@@ -338,16 +343,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (; kb < kb1; ++kb) {
           if (!wait_full(stage, phase)) { ok = false; break; }
-          if (tl && tl_first && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
+          if (tl && lane == 0 && tl_first && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
           issue(d_tmem, stage, kb == kb0, 0, NT);
           // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
           // in the other pair, whose producers multicast into this pair's slots
-          tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+          if (lane == 0) tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+          __syncwarp();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
         if (!ok) break;
-        if (tl && j < 8) tl[4 * j + 1] = globaltimer_ns();
-        tc_commit<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs of the pair)
+        if (tl && lane == 0 && j < 8) tl[4 * j + 1] = globaltimer_ns();
+        if (lane == 0) tc_commit<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs)
+        __syncwarp();
       }
     }
   } else {
