@@ -564,6 +564,28 @@ def test_config3_bf16_16384(mm):
     print(f"C4 bf16 sampled max normalized error: rows {e1:.3e} cols {e2:.3e}")
 
 
+def test_config3_row_blocks_bit_identical(mm):
+    """C4 at full size in the configuration bench.py times: the row blocks of the 2-, 4- and
+    8-GPU row-block sharding (mm_shard_range), each multiplied on its own as a rank would, equal
+    the single-GPU product bit for bit on the config's own Box-Muller bf16 inputs (on-GPU
+    generator, bit-identical to synthgen)."""
+    from synthgen import gpu as sgg
+    N = 16384
+    A = sgg.normal_bf16(3, sg.ROLE_A, N, N)
+    B = sgg.normal_bf16(3, sg.ROLE_B, N, N)
+    full = mm.gemm(A, B)
+    mm.sync_check()
+    for G in (2, 4, 8):
+        for r in range(G):
+            r0, rows = mm.shard_range(N, G, r)
+            blk = mm.gemm(A[r0:r0 + rows].contiguous(), B)
+            mm.sync_check()
+            assert torch.equal(blk, full[r0:r0 + rows]), (G, r)
+            del blk
+    del full
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("K", [3, 9])
 def test_config3_bf16_16384_exact_pins(mm, K):
     key = f"C4x{K}"
