@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;  // rank in the cluster (CG*MC CTAs)
+  // warp-uniform by construction (__shfl_sync): lets the compiler keep role branches and operand
+  // arithmetic in uniform registers (no per-instruction waterfalls around tcgen05 / TMA operands)
+  const uint32_t crank = (CG == 2) ? __shfl_sync(0xffffffffu, cluster_ctarank(), 0) : 0u;  // rank in the cluster
   const uint32_t rank = crank & (uint32_t)(CG - 1);            // rank in the CTA pair
   const uint32_t pair = crank / (uint32_t)CG;                   // pair index along M (MC = 2)
   const uint32_t leader = crank - rank;                         // the pair's MMA-issuing CTA
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   // optional timeline (MM_TRACE=1): per CTA ns spent waiting, by role
   uint64_t tr_barrier = 0, tr_empty = 0, tr_tempty = 0, tr_full = 0, tr_tfull = 0, tr_drain = 0;
   uint64_t tr_c[5] = {0, 0, 0, 0, 0};  // epilogue per-chunk cycles: ld-wait, st.shared, fence, store, chunks
