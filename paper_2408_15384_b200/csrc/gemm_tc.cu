@@ -38,24 +38,28 @@ namespace {
 constexpr int kThreads = 320;  // warp 0 TMA producer, warp 1 TMEM + MMA issuer, warps 2..9 epilogue
 constexpr int kBN = 256;  // MMA N (columns of C per tile)
 
-template <bool I8, int CG, int NT, int MC = 1>
+// KA: 128-B swizzle atoms of K per stage (2: twice the MMAs per barrier wait and commit)
+template <bool I8, int CG, int NT, int MC = 1, int KA = 1>
 struct TcCfg {
   static constexpr int ESZ = I8 ? 1 : 2;
-  static constexpr int BK = 128 / ESZ;        // K elements per stage (one 128-B swizzle atom)
+  static constexpr int BKA = 128 / ESZ;       // K elements per 128-B swizzle atom (one A box)
+  static constexpr int BK = BKA * KA;         // K elements per stage
   static constexpr int UK = I8 ? 32 : 16;     // K per tcgen05.mma
-  static constexpr int KSTEPS = BK / UK;      // 4
+  static constexpr int KSTEPS = BK / UK;      // 4 per atom
+  static constexpr int KPA = BKA / UK;        // K steps per atom
   static constexpr int BM = 128;              // rows of A per CTA
   static constexpr int TILE_N = kBN * NT;     // columns of C per tile (NT accumulators of N=256)
   static constexpr int NBUF = (NT == 1) ? 2 : 1;  // TMEM accumulator buffers: NBUF * TILE_N = 512 columns
   static constexpr int BN_CTA = kBN / CG;     // columns of B per CTA per MMA region
   static constexpr int BOXN = 128 / ESZ;      // columns per TMA box of B (128 B)
   static constexpr int NBOX = BN_CTA / BOXN;  // boxes per region
-  static constexpr int A_BYTES = BM * 128;
+  static constexpr int A_ATOM = BM * 128;     // one A box
+  static constexpr int A_BYTES = A_ATOM * KA;
   static constexpr int BOX_BYTES = BK * 128;
   static constexpr int REGION_BYTES = NBOX * BOX_BYTES;
   static constexpr int B_BYTES = NT * REGION_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 1 || NT == 2) ? 4 : 6;
+  static constexpr int STAGES = KA == 2 ? 3 : ((CG == 1 || NT == 2) ? 4 : 6);
   static constexpr int EPI_BYTES = 8 * 32 * 128;  // epilogue staging: 8 warps x (32 rows x 128 B)
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static constexpr int M_MMA = 128 * CG;
@@ -114,11 +118,11 @@ __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict
   add_words<I8>(v, w);
 }
 
-template <bool I8, int CG, int NT, int MC>
+template <bool I8, int CG, int NT, int MC, int KA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
-  using Cfg = TcCfg<I8, CG, NT, MC>;
+  using Cfg = TcCfg<I8, CG, NT, MC, KA>;
   const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
   // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
   unsigned long long* tl = args.trace ? args.trace + 4096 * 16 + (size_t)blockIdx.x * 32 : nullptr;
@@ -253,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d_pair_hint(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
                                       n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
             } else {
-              tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+#pragma unroll
+              for (int a = 0; a < KA; ++a)
+                tma_load_2d_pair(sa + a * Cfg::A_ATOM, &tmA, leader_full, k0 + a * Cfg::BKA, m0);
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_pair(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
           // A: K-major SW128, rows 128 B apart, 8-row groups 1024 B apart (SBO); K step = 32 B.
-          const uint64_t adesc = umma_desc_sw128(sa + kk * 32, 16, 1024);
+          const uint64_t adesc = umma_desc_sw128(sa + (kk / Cfg::KPA) * Cfg::A_ATOM + (kk % Cfg::KPA) * 32, 16, 1024);
 #pragma unroll
           for (int rr = 0; rr < NT; ++rr) {
             if (rr < r0 || rr >= r1) continue;
@@ -563,9 +569,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // max_clusters: how many clusters of cg*mc CTAs can be co-resident (the persistent grid and the
 // wave barrier need all of them resident at once); <= 0: num_sms / (cg*mc).
-WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, int max_clusters) {
+WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, int max_clusters,
+                     int ka = 1) {
   const int m_mma = 128 * cg * mc;
-  const int bk = i8 ? 128 : 64;
+  const int bk = (i8 ? 128 : 64) * ka;
   const int tiles_m = (int)((M + m_mma - 1) / m_mma);
   const int tiles_n = (int)((N + kBN * nt - 1) / (kBN * nt));
   // measured best (tools/sweep_raster.py): 256-wide tiles 8 tile-rows x ~9 tile-cols per 74-cluster wave;
@@ -593,10 +600,10 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)nc, mode);
 }
 
-template <bool I8, int CG, int NT, int MC>
+template <bool I8, int CG, int NT, int MC, int KA = 1>
 cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int num_sms, int* max_clusters) {
-  using Cfg = TcCfg<I8, CG, NT, MC>;
-  auto kern = gemm_tc_kernel<I8, CG, NT, MC>;
+  using Cfg = TcCfg<I8, CG, NT, MC, KA>;
+  auto kern = gemm_tc_kernel<I8, CG, NT, MC, KA>;
   // per template instance and device (function attributes and occupancy are per device)
   static std::atomic<int> max_cl_dev[kMaxDevices];  // 0 = not set up yet, -1 = query failed
   int dev = 0;
@@ -632,18 +639,18 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
   return cudaSuccess;
 }
 
-template <bool I8, int CG, int NT, int MC>
+template <bool I8, int CG, int NT, int MC, int KA = 1>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
                         int num_sms, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[2];
   int max_cl = 0;
-  cudaError_t e = launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl);
+  cudaError_t e = launch_cfg<I8, CG, NT, MC, KA>(cfg, attr, num_sms, &max_cl);
   if (e != cudaSuccess) return e;
-  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl);
+  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA);
   cfg.gridDim = dim3(sched.nc * CG * MC, 1, 1);
   cfg.stream = s;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC>, tmA, tmB, tmC, a, sched);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, a, sched);
 }
 
 template <bool I8, int CG, int NT, int MC>
@@ -669,18 +676,18 @@ int max_clusters_impl(bool i8, int cg, int nt, int mc, int num_sms) {
 
 int max_clusters(bool i8, int cg, int nt, int mc, int num_sms) { return max_clusters_impl(i8, cg, nt, mc, num_sms); }
 
-void tc_box_dims(bool i8, int cg, int mc, uint32_t* a_box, uint32_t* b_box) {
+void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box, uint32_t* b_box) {
   const uint32_t esz = i8 ? 1 : 2;
   a_box[0] = 128 / esz;       // K elements (128 B)
   a_box[1] = 128;             // rows
   b_box[0] = 128 / esz;       // N elements (128 B)
-  b_box[1] = 128 / esz / mc;  // K rows (BK, or the half of it one pair loads when two pairs share B)
+  b_box[1] = 128 / esz * ka / mc;  // K rows (BK, or the half of it one pair loads when two pairs share B)
   (void)cg;
 }
 
-void tc_plan_needs(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
-                   size_t* flag_count) {
-  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, num_sms));
+void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N, int64_t K, int num_sms,
+                   size_t* ws_bytes, size_t* flag_count) {
+  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, num_sms), ka);
   *ws_bytes = (size_t)sc.ntc * cg * mc * 128 * kBN * nt * 4;
   *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc;
 }
@@ -697,6 +704,9 @@ cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& t
     return nt == 2 ? launch_impl<false, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
                    : launch_impl<false, 2, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
   }
+  if (nt == 1 && a.ka == 2)
+    return i8 ? launch_impl<true, 2, 1, 1, 2>(tmA, tmB, tmC, a, num_sms, s)
+              : launch_impl<false, 2, 1, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
   if (i8)
     return nt == 2 ? launch_impl<true, 2, 2, 1>(tmA, tmB, tmC, a, num_sms, s)
                    : launch_impl<true, 2, 1, 1>(tmA, tmB, tmC, a, num_sms, s);

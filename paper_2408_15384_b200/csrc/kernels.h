@@ -27,6 +27,7 @@ struct GemmArgs {
   int l2_hint;      // tcgen05 kernel: TMA loads of A evict_last, of B evict_first
   unsigned long long* trace;  // optional per-CTA wait-time counters (16 per CTA), MM_TRACE=1
   int debug;        // diagnostics only (MM_DEBUG): bit 0 = tcgen05 producer skips the operand loads
+  int ka;           // tcgen05 kernel: 128-B K atoms per stage (1, or 2 for 256-wide pair tiles)
 };
 
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).
@@ -47,10 +48,10 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms);
 cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s);
 // Workspace (stream-K partial slabs) and per-tile counters the launch will use.
-void tc_plan_needs(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, size_t* ws_bytes,
-                   size_t* flag_count);
+void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N, int64_t K, int num_sms,
+                   size_t* ws_bytes, size_t* flag_count);
 // Box extents the tensor maps must be encoded with.
-void tc_box_dims(bool i8, int cg, int mc, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
+void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
 // Co-resident clusters of the given configuration (0 if the query failed).
 int max_clusters(bool i8, int cg, int nt, int mc, int num_sms);
 

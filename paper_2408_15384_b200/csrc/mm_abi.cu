@@ -219,6 +219,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.l2_hint = 0;
   a.trace = nullptr;
   a.debug = 0;
+  a.ka = 1;
   if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
@@ -311,15 +312,23 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     // 16384, 3.46 waves of 512-wide tiles vs 6.92 of 256-wide ones) runs 6 % faster at NT=2.
     const int64_t tiles_nt2 = ((m + 255) / 256) * ((p + 511) / 512);
     int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= ctx->num_sms / 2)) ? 2 : 1;
-    if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // two CTA pairs per cluster sharing (multicasting) every B slab
     int mc = 1;
     if (const char* env = knob("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    // With few waves of 512-wide tiles (quantisation, an exposed read-out per tile) 256-wide tiles
+    // with TMEM double-buffering and two K atoms per stage win: int8 4096^3 +3 %, bf16 4096^3 +2 %;
+    // from ~7 waves on (8192^3) 512-wide tiles stay ahead (tools/ab_gpu.py).
+    if (nt == 2 && !a.wave_sync && mc == 1 && tiles_nt2 < 3 * (ctx->num_sms / 2)) nt = 1;
+    if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    // 256-wide pair tiles: two 128-B K atoms per stage — 8 MMAs per barrier wait and commit instead
+    // of 4 (the single issuing thread, not the tensor pipe, bounded 4-MMA stages at ~75 % busy)
+    a.ka = (cg == 2 && nt == 1 && mc == 1 && n >= 8 * (i8 ? 128 : 64)) ? 2 : 1;
+    if (const char* env = knob("MM_KA")) a.ka = (cg == 2 && nt == 1 && mc == 1 && atoi(env) == 2) ? 2 : 1;
     size_t ws_bytes = 0, flag_count = 0;
-    tc_plan_needs(i8, cg, nt, mc, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
+    tc_plan_needs(i8, cg, nt, mc, a.ka, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
     mm_status st = ensure_sk(ws_bytes, flag_count);
     if (st != MM_OK) return st;
-    tc_box_dims(i8, cg, mc, abox, bbox);
+    tc_box_dims(i8, cg, mc, a.ka, abox, bbox);
     const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
     if (st != MM_OK) return st;
