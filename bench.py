@@ -44,6 +44,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GEMM TFLOPS (2mnp/s) per dtype at 1/2/4/8 B200; fraction of dense peak"
 UNIT = "TFLOP/s"
+# dense flop (int op) per clock per SM: the HGX-B200 spec peaks
+# (2.25 PF BF16, 4.5 P INT8, 37 TF FP64) over 148 SMs at ~1.86 / 1.86 / 1.95 GHz
+OPS_PER_CLK_SM = {"bf16": 8192, "i8": 16384, "f64": 128}
 M = N_ = P = 16384
 SEED = 3
 WORKLOAD = ("BASELINE.json configs[3]: BF16 16384x16384 . 16384x16384, FP32 accumulate and output, "
@@ -205,6 +208,28 @@ def per_config_table(mm, peaks):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     out = {}
     bf16_peak = peaks["bf16_tflops"]
+    SMS = torch.cuda.get_device_properties(0).multi_processor_count
+    # measured library peaks, cuBLAS at 8192^3 (operands larger than L2)
+    lib_peaks = {}
+    for dt, tin in (("f64", torch.float64), ("i8", torch.int8)):
+        try:
+            if dt == "f64":
+                X = torch.rand(8192, 8192, dtype=tin, device="cuda")
+                Y = torch.rand(8192, 8192, dtype=tin, device="cuda")
+                f = lambda: torch.matmul(X, Y)  # noqa: E731
+            else:
+                X = torch.randint(-127, 128, (8192, 8192), dtype=tin, device="cuda")
+                Y = torch.randint(-127, 128, (8192, 8192), dtype=tin, device="cuda")
+                f = lambda: torch._int_mm(X, Y)  # noqa: E731
+            for _ in range(3):
+                f()
+            lib_peaks[dt] = 2.0 * 8192 ** 3 / per_launch_ms(f, 5 if dt == "f64" else 20) / 1e9
+            del X, Y
+        except Exception:  # noqa: BLE001
+            pass
+    out["library_peaks"] = {"fp64_cublas_8192_tflops": round(lib_peaks.get("f64", 0.0), 2) or None,
+                            "int8_cublas_8192_tops": round(lib_peaks.get("i8", 0.0), 2) or None,
+                            "how": "torch.matmul float64 / torch._int_mm at 8192^3, per-launch medians"}
     cases = [
         ("configs[0] FP64 256^3 seed 0", "f64", 256, 256, 256, 0, 30),
         ("configs[1] FP64 2000x1500x1750 seed 1", "f64", 2000, 1500, 1750, 1, 15),
@@ -228,10 +253,20 @@ def per_config_table(mm, peaks):
             C = torch.empty(m, p, device="cuda", dtype=torch.float64 if dt == "f64" else torch.int32)
             flops = 2.0 * m * n * p
             big = m * n > (1 << 26)
+            ck = ClockSampler()
+            ck.start()
             t_ours = per_launch_ms(lambda: mm.gemm(A, B, out=C), reps, None if big else flush)
+            clk_ours = ck.stop()
             mm.sync_check()
+            ck = ClockSampler()
+            ck.start()
             t_ref = per_launch_ms(ref, reps, None if big else flush)
+            clk_ref = ck.stop()
             tf = flops / t_ours / 1e9
+            # SMs x flop/clk/SM x the SM clock sampled while it ran
+            opc = OPS_PER_CLK_SM["f64" if dt == "f64" else "i8"]
+            clock_peak = (SMS * opc * clk_ours["sm_mhz"] * 1e6 / 1e12) if clk_ours else None
+            lib = lib_peaks.get(dt)
             graph = None
             if m * n * p <= (1 << 27):
                 # launch-amortised: 100 products captured in one CUDA graph
@@ -241,6 +276,10 @@ def per_config_table(mm, peaks):
                 "ms": round(t_ours, 4), "tflops": round(tf, 2), "frac_of_peak": round(tf / nominal, 4),
                 "graph_batch_100": graph,
                 "peak": round(nominal, 1), "peak_note": peak_note,
+                "frac_of_library_peak": round(tf / lib, 4) if lib else None,
+                "frac_of_clock_peak": round(tf / clock_peak, 4) if clock_peak else None,
+                "sm_mhz": clk_ours["sm_mhz"] if clk_ours else None,
+                "cublas_sm_mhz": clk_ref["sm_mhz"] if clk_ref else None,
                 "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
                 "l2": "flushed before each launch" if not big else "operands larger than L2",
             }
@@ -491,7 +530,13 @@ def main():
             "protocol": protocol,
             "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
                                        "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
-                                       "vs_spec_2250": round(value / world / 2250.0, 4)},
+                                       "vs_spec_2250": round(value / world / 2250.0, 4),
+                                       "vs_clock_normalized": (round(value / world / (
+                                           torch.cuda.get_device_properties(0).multi_processor_count *
+                                           OPS_PER_CLK_SM["bf16"] * clocks["sm_mhz"] * 1e6 / 1e12), 4)
+                                           if clocks else None),
+                                       "clock_normalized_note": "SMs x 8192 flop/clk x median nvidia-smi SM clock "
+                                                                "of the timed region"},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -383,10 +383,11 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
 F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   F64Plan pl;
   auto tiles = [&](int b) { return ((M + b - 1) / b) * ((N + b - 1) / b); };
-  // 128x128 when there is at least a wave of them; else 32x32 when those fit one wave (every
-  // CTA one whole tile, no fix-up: C1 = 64 tiles); else 64x64 (measured: 512^3 20.5 us at 64x64
-  // split vs 26.6 us at 32x32 split, tools/ab_gpu.py).
-  pl.bm = pl.bn = tiles(128) >= num_sms ? 128 : (tiles(32) <= num_sms ? 32 : 64);
+  // 128x128 from ~0.6 of a wave of them (16-warp kernels, tools/ab_gpu.py: 96 tiles +2.5 %,
+  // 81 even, 64 -5 % vs 64x64); else 32x32 when those fit one wave (every CTA one whole tile,
+  // no fix-up: C1 = 64 tiles); else 64x64 (measured: 512^3 20.5 us at 64x64 split vs 26.6 us
+  // at 32x32 split).
+  pl.bm = pl.bn = 5 * tiles(128) >= 3 * num_sms ? 128 : (tiles(32) <= num_sms ? 32 : 64);
   if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 128
     const int v = atoi(e);
     if (v == 32 || v == 64 || v == 128) pl.bm = pl.bn = v;
@@ -432,8 +433,17 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
 
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                             const CUtensorMap& tmB3, const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
-  if (pl.bm == 128) return launch_impl<128, 128, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
-  if (pl.bm == 64) return launch_impl<64, 64, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  if (pl.bm == 128) {
+    // 16 consumer warps of 32x32 (4 per SM sub-partition, ~96 registers): a warp stalled at a k-block
+    // boundary or on a fragment load leaves three others to keep the DMMA pipe busy.  8 warps of
+    // 64x32 (MM_F64_W8=1) kept it ~93.6 % busy; 16 warps +2-3 % (C2 344 -> 334 us, 8192^3 31.6 -> 30.9 ms)
+    if (knob("MM_F64_W8")) return launch_impl<128, 128, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);  // (A/B knob)
+    return launch_impl<128, 128, 4, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  }
+  if (pl.bm == 64) {  // 16 warps of 16x16 (8 of 32x16 with MM_F64_W8=1): +2-11 % at 512^3-1024^3
+    if (knob("MM_F64_W8")) return launch_impl<64, 64, 2, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);  // (A/B knob)
+    return launch_impl<64, 64, 4, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
+  }
   if (pl.kb > 1) {  // 32x32, grouped loads (KB = 4 k-blocks per TMA load)
     if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);
     return launch_impl<32, 32, 2, 2, 1, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);

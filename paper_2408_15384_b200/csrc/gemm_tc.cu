@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // prefetch) overlapped the previous kernel in the stream; no global memory is touched before
       // it has completed (the MMA and epilogue only run on data loaded after this wait).
       pdl_wait();
+      if (args.trace) args.trace[(size_t)blockIdx.x * 16 + 15] = globaltimer_ns();
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         // Wave barrier: start item j only when every CTA has issued all loads of its
         // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
@@ -240,7 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // to the same-rank CTA of both pairs (which need the same B columns).
             const uint32_t leader_full = mapa_shared(full_bar(stage), leader);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
-            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+#pragma unroll
+            for (int a = 0; a < KA; ++a)
+              tma_load_2d_pair(sa + a * Cfg::A_ATOM, &tmA, leader_full, k0 + a * Cfg::BKA, m0);
             const uint16_t mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
 #pragma unroll
             for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
@@ -653,17 +656,21 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, a, sched);
 }
 
-template <bool I8, int CG, int NT, int MC>
+template <bool I8, int CG, int NT, int MC, int KA = 1>
 int max_clusters_of(int num_sms) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[2];
   int max_cl = 0;
-  if (launch_cfg<I8, CG, NT, MC>(cfg, attr, num_sms, &max_cl) != cudaSuccess) return 0;
+  if (launch_cfg<I8, CG, NT, MC, KA>(cfg, attr, num_sms, &max_cl) != cudaSuccess) return 0;
   return max_cl;
 }
 
-int max_clusters_impl(bool i8, int cg, int nt, int mc, int num_sms) {
+int max_clusters_impl(bool i8, int cg, int nt, int mc, int ka, int num_sms) {
   if (cg == 1) return i8 ? max_clusters_of<true, 1, 1, 1>(num_sms) : max_clusters_of<false, 1, 1, 1>(num_sms);
+  if (nt == 1 && ka == 2) {
+    if (mc == 2) return i8 ? max_clusters_of<true, 2, 1, 2, 2>(num_sms) : max_clusters_of<false, 2, 1, 2, 2>(num_sms);
+    return i8 ? max_clusters_of<true, 2, 1, 1, 2>(num_sms) : max_clusters_of<false, 2, 1, 1, 2>(num_sms);
+  }
   if (mc == 2) {
     if (i8) return nt == 2 ? max_clusters_of<true, 2, 2, 2>(num_sms) : max_clusters_of<true, 2, 1, 2>(num_sms);
     return nt == 2 ? max_clusters_of<false, 2, 2, 2>(num_sms) : max_clusters_of<false, 2, 1, 2>(num_sms);
@@ -674,7 +681,7 @@ int max_clusters_impl(bool i8, int cg, int nt, int mc, int num_sms) {
 
 }  // namespace
 
-int max_clusters(bool i8, int cg, int nt, int mc, int num_sms) { return max_clusters_impl(i8, cg, nt, mc, num_sms); }
+int max_clusters(bool i8, int cg, int nt, int mc, int ka, int num_sms) { return max_clusters_impl(i8, cg, nt, mc, ka, num_sms); }
 
 void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box, uint32_t* b_box) {
   const uint32_t esz = i8 ? 1 : 2;
@@ -687,7 +694,7 @@ void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box, uint32_t* b_b
 
 void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N, int64_t K, int num_sms,
                    size_t* ws_bytes, size_t* flag_count) {
-  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, num_sms), ka);
+  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, ka, num_sms), ka);
   *ws_bytes = (size_t)sc.ntc * cg * mc * 128 * kBN * nt * 4;
   *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc;
 }
@@ -697,6 +704,9 @@ cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& t
   if (cg == 1)
     return i8 ? launch_impl<true, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s)
               : launch_impl<false, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+  if (mc == 2 && nt == 1 && a.ka == 2)
+    return i8 ? launch_impl<true, 2, 1, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
+              : launch_impl<false, 2, 1, 2, 2>(tmA, tmB, tmC, a, num_sms, s);
   if (mc == 2) {
     if (i8)
       return nt == 2 ? launch_impl<true, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)

@@ -53,7 +53,7 @@ void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N
 // Box extents the tensor maps must be encoded with.
 void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box /*[2]*/, uint32_t* b_box /*[2]*/);
 // Co-resident clusters of the given configuration (0 if the query failed).
-int max_clusters(bool i8, int cg, int nt, int mc, int num_sms);
+int max_clusters(bool i8, int cg, int nt, int mc, int ka, int num_sms);
 
 // FP64 on DMMA (mma.sync m8n8k4) with TMA-fed smem ring.
 // tmA3 / tmB3: the 3-D slab maps used when pl.kb > 1 (A {16, m, n/16} box {16, bm, kb};

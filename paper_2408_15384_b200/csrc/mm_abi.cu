@@ -322,8 +322,8 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // 256-wide pair tiles: two 128-B K atoms per stage — 8 MMAs per barrier wait and commit instead
     // of 4 (the single issuing thread, not the tensor pipe, bounded 4-MMA stages at ~75 % busy)
-    a.ka = (cg == 2 && nt == 1 && mc == 1 && n >= 8 * (i8 ? 128 : 64)) ? 2 : 1;
-    if (const char* env = knob("MM_KA")) a.ka = (cg == 2 && nt == 1 && mc == 1 && atoi(env) == 2) ? 2 : 1;
+    a.ka = (cg == 2 && nt == 1 && n >= 8 * (i8 ? 128 : 64)) ? 2 : 1;
+    if (const char* env = knob("MM_KA")) a.ka = (cg == 2 && nt == 1 && atoi(env) == 2) ? 2 : 1;
     size_t ws_bytes = 0, flag_count = 0;
     tc_plan_needs(i8, cg, nt, mc, a.ka, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
     mm_status st = ensure_sk(ws_bytes, flag_count);
@@ -348,7 +348,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, a, ctx->num_sms, s);
     trace_nt = nt;
     trace_mc = mc;
-    if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, ctx->num_sms);
+    if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, a.ka, ctx->num_sms);
   }
   if (e == cudaSuccess) ++ctx->launches;
   if (e == cudaSuccess && trace) {
@@ -378,19 +378,25 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
         if (h[(size_t)c * 16 + 14]) e0 = std::min(e0, h[(size_t)c * 16 + 14]);
       double acc[32] = {0};
       int cnt[32] = {0};
-      double ent = 0;
+      double ent = 0, setup = 0, pdl = 0, ex = 0, exmax = 0;
       int nent = 0;
       for (int c = 0; c < 4096; ++c) {
         const unsigned long long* r = &h[(size_t)c * 16];
         const unsigned long long* tlc = &h[4096 * 16 + (size_t)c * 32];
         if (!r[6]) continue;
         ent += (double)(r[14] - e0);
+        setup += (double)(r[6] - e0);
+        if (r[15]) pdl += (double)(r[15] - e0);
+        ex += (double)(r[7] - e0);
+        exmax = std::max(exmax, (double)(r[7] - e0));
         ++nent;
         for (int k = 0; k < 32; ++k)
           if (tlc[k]) { acc[k] += (double)(tlc[k] - e0); ++cnt[k]; }
       }
       if (nent) {
-        fprintf(stderr, "[mm trace] timeline (us after first CTA entry, CTA average): entry %.2f", 1e-3 * ent / nent);
+        fprintf(stderr, "[mm trace] timeline (us after first CTA entry, CTA average): entry %.2f setup %.2f pdl-wait %.2f "
+                "exit %.2f (last %.2f)", 1e-3 * ent / nent, 1e-3 * setup / nent, 1e-3 * pdl / nent, 1e-3 * ex / nent,
+                1e-3 * exmax);
         for (int j = 0; j < 8; ++j)
           if (cnt[4 * j])
             fprintf(stderr, " | item %d: MMA %.2f-%.2f epi %.2f-%.2f (%d)", j, 1e-3 * acc[4 * j] / cnt[4 * j],

@@ -250,13 +250,16 @@ def test_f64_tiles_and_schedules(mm, tile, streamk):
 
 
 @pytest.mark.parametrize("dt", ["i8", "bf16"])
-@pytest.mark.parametrize("nt", ["1", "2"])
-def test_cluster_multicast_mc2(mm, dt, nt):
+@pytest.mark.parametrize("nt,ka", [("1", None), ("1", "1"), ("2", None)])
+def test_cluster_multicast_mc2(mm, dt, nt, ka):
     """Clusters of two CTA pairs (512-row tiles) sharing every B slab by TMA multicast, each
     pair loading half of its K rows: ragged m (partial second pair), ragged n and p, and a
-    guard-banded C (no store outside C)."""
+    guard-banded C (no store outside C).  256-wide tiles with one or (default for n >= 8 atoms)
+    two K atoms per stage."""
     os.environ["MM_MC"] = "2"
     os.environ["MM_NT"] = nt
+    if ka:
+        os.environ["MM_KA"] = ka
     try:
         for (m, n, p) in [(300, 200, 520), (513, 1024, 1100), (1100, 768, 1700), (2048, 2048, 2048), (777, 64, 300)]:
             A, B = gen(dt, "exact", 44, m, n, p, 255 if dt == "i8" else 9)
@@ -280,6 +283,7 @@ def test_cluster_multicast_mc2(mm, dt, nt):
     finally:
         os.environ.pop("MM_MC", None)
         os.environ.pop("MM_NT", None)
+        os.environ.pop("MM_KA", None)
 
 
 @pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])

@@ -20,7 +20,18 @@ else:
     A = torch.randn(m, n, device="cuda").to(tin)
     B = torch.randn(n, p, device="cuda").to(tin)
 C = torch.empty(m, p, dtype=tout, device="cuda")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
 for _ in range(reps):
-    mm.gemm(A, B, out=C)
+    if flush is not None:
+        flush.fill_(1)  # (FLUSH=1: L2 full of other data before every call)
+    if os.environ.get("LIB"):  # (LIB=1: the cuBLAS product on the same operands instead)
+        if dt == "i8":
+            torch._int_mm(A, B, out=C)
+        elif dt == "bf16":
+            torch.mm(A, B, out_dtype=torch.float32, out=C)
+        else:
+            torch.mm(A, B, out=C)
+    else:
+        mm.gemm(A, B, out=C)
 mm.sync_check()
 print("ok", dt, m, n, p)
