@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
 #pragma unroll
         for (int ni = 0; ni < Cfg::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
+      // (MM_TRACE: first stage landed — checked here, not in the k-loop, where the trace pointer
+      // cost a local-memory reload and a branch per k-block)
+      if (tl && warp == 0 && j == 0 && mbar_wait(full_bar(stage), phase, err, 12) && lane == 0) tl[3] = globaltimer_ns();
       for (int kb = kb0; kb < kb1; kb += KB) {
         const int nk = min(KB, kb1 - kb);  // k-blocks in this group (KB == 1: one)
         if (KB == 1 && KS > 1 && (int)(gk % KS) != kgrp) {  // the other warp group's k-block
@@ -200,7 +203,6 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
           continue;
         }
         if (!mbar_wait(full_bar(stage), phase, err, 12)) { ok = false; break; }
-        if (tl && warp == 0 && lane == 0 && j == 0 && kb == kb0) tl[3] = globaltimer_ns();
         for (int i = 0; i < nk; ++i) {
         if (KB > 1 && KS > 1 && (int)((gk + i) % KS) != kgrp) continue;  // the other warp group's k-block
         // slot (stage + i): A slab at its own slot; B (KB > 1) at the group's B region, k-block i
