@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // out TMA, straight from registers with predicated stores.
     const uint32_t ebuf = sEpi + ew * 4096u;
     uint32_t n_stores = 0;
-    auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0) {
+    auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0, bool red = false) {
       if (args.c_tma) {
         const uint64_t c0 = args.trace ? clock64() : 0;
         if (n_stores >= 1) {
@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         const uint64_t c3 = args.trace ? clock64() : 0;
         if (lane == 0 && !(args.debug & 4)) {  // (diagnostics: bit 2 skips the store)
-          tma_store_2d(&tmC, ebuf, (int32_t)col0, (int32_t)row_base);
+          if (red) tma_reduce_add_2d(&tmC, ebuf, (int32_t)col0, (int32_t)row_base);
+          else tma_store_2d(&tmC, ebuf, (int32_t)col0, (int32_t)row_base);
           bulk_commit();
         }
         if (args.trace) {
@@ -434,6 +435,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       sched.tile_coords(t, tm, tn);
       const int acc = j % Cfg::NBUF;
       const uint32_t use = (uint32_t)(j / Cfg::NBUF);
+      // reduce-add tail (sched.red): the half holding k-block 0 zeroes this CTA's rows of the tile in C
+      // while its MMAs run, then publishes that; both halves later add into C with TMA reduce-add
+      const bool red_item = sched.red && !(kb0 == 0 && kb1 == num_kb);
+      unsigned* red_flag = args.flags + (size_t)t * (CG * MC) + crank;
+      if (red_item && kb0 == 0) {
+        const int64_t zrow = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + q * 32;
+        if (n_stores >= 1) {
+          if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the buffer
+          __syncwarp();
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st_shared_v4(ebuf + lane * 128u + (uint32_t)i * 16u, 0u, 0u, 0u, 0u);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int c = h; c < NCH; c += 2) tma_store_2d(&tmC, ebuf, (int32_t)((int64_t)tn * Cfg::TILE_N + c * 32), (int32_t)zrow);
+          bulk_commit();
+          bulk_wait<0>();  // the zeros are in global memory
+        }
+        ++n_stores;
+        __syncwarp();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before the release
+          red_release_gpu_add(red_flag, 1u);
+        }
+      }
       const uint64_t tq0 = args.trace ? globaltimer_ns() : 0;
       if (!mbar_wait(tfull_bar(acc), use & 1u, err, 4)) break;
       if (args.trace) tr_tfull += globaltimer_ns() - tq0;
@@ -446,7 +474,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tail_c = cl;  // tail items: cluster index == tail-slot index
       const int64_t row_base = row - lane;  // first row of this warp's 32-row block
       const int64_t col_t = (int64_t)tn * Cfg::TILE_N;
-      if (whole) {
+      if (red_item) {
+        if (kb0 != 0) {
+          // wait until the partner half has zeroed these rows (and reset its flag for the next launch)
+          if (ew == 0 && lane == 0) {
+            if (counter_wait(red_flag, 1u, err, 8)) *(volatile unsigned*)red_flag = 0u;
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired zeros before the reduce-adds
+          }
+          __syncwarp();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
+#pragma unroll 1
+        for (int c = h; c < NCH; c += 2) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+          emit(v, row_base, col_t + c * 32, true);
+        }
+      } else if (whole) {
         // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
         uint32_t va[32], vb[32];
         tmem_ld_32x32b_x32(t_row + h * 32, va);
@@ -573,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // max_clusters: how many clusters of cg*mc CTAs can be co-resident (the persistent grid and the
 // wave barrier need all of them resident at once); <= 0: num_sms / (cg*mc).
 WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int64_t K, int num_sms, int max_clusters,
-                     int ka = 1) {
+                     int ka = 1, bool c_tma = true) {
   const int m_mma = 128 * cg * mc;
   const int bk = (i8 ? 128 : 64) * ka;
   const int tiles_m = (int)((M + m_mma - 1) / m_mma);
@@ -596,10 +641,19 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // the general split (partials read from global memory), MM_STREAMK=0 disables both.
   // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
   // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
-  int mode = (!i8 && tail > 0 && nt == 1 && mc == 1 && 2 * tail <= nc && num_kb >= 8) ? 2 : 0;
+  // Mode 3 (when C takes TMA stores): the same exact halves, both added into C (zeroed by
+  // the first half while its MMAs run) with TMA reduce-add stores — no partial slabs, no
+  // read-back, neither half waits for the other's MMAs.
+  // Reduce-add stores take ~1.5x as long as plain ones and the zeroing half stores the tile twice,
+  // so int8 (half-length tiles) gains only with long K (C3: 16 k-blocks, neutral; 2560^3 -7 %),
+  // bf16 from 4 k-blocks on (4096^3 +4 %, 2560^3 +5 % over landing, tools/ab_gpu.py).
+  int mode = 0;
+  if (tail > 0 && mc == 1 && 2 * tail <= nc && num_kb >= (i8 ? 24 : 4))
+    mode = c_tma ? 3 : ((!i8 && nt == 1 && num_kb >= 8) ? 2 : 0);
   if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
   if (mode == 2 && (nt != 1 || 2 * tail > nc)) mode = 1;  // landing: 256-wide tiles, one partner per tile
+  if (mode == 3 && (!c_tma || 2 * tail > nc)) mode = 1;
   return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)nc, mode);
 }
 
@@ -650,7 +704,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   int max_cl = 0;
   cudaError_t e = launch_cfg<I8, CG, NT, MC, KA>(cfg, attr, num_sms, &max_cl);
   if (e != cudaSuccess) return e;
-  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA);
+  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA, a.c_tma != 0);
   cfg.gridDim = dim3(sched.nc * CG * MC, 1, 1);
   cfg.stream = s;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, a, sched);
@@ -694,8 +748,10 @@ void tc_box_dims(bool i8, int cg, int mc, int ka, uint32_t* a_box, uint32_t* b_b
 
 void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N, int64_t K, int num_sms,
                    size_t* ws_bytes, size_t* flag_count) {
-  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, max_clusters_impl(i8, cg, nt, mc, ka, num_sms), ka);
-  *ws_bytes = (size_t)sc.ntc * cg * mc * 128 * kBN * nt * 4;
+  const int mcl = max_clusters_impl(i8, cg, nt, mc, ka, num_sms);
+  const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, mcl, ka, true);
+  const WorkSched sc2 = make_sched(i8, cg, nt, mc, M, N, K, num_sms, mcl, ka, false);  // (C without TMA stores)
+  *ws_bytes = (size_t)std::max(sc.ntc, sc2.ntc) * cg * mc * 128 * kBN * nt * 4;
   *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc;
 }
 

@@ -22,6 +22,7 @@ struct WorkSched {
   int W;     // full data-parallel waves
   int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
   int land;  // tail tiles split in exact halves: the finisher lands the partner's slab in its idle stage ring
+  int red;   // tail tiles split in exact halves, both adding into C (zeroed first) by TMA reduce-add stores
   int64_t TI;  // tail iterations = tail tiles * num_kb
 
   __device__ __forceinline__ void tile_coords(int t, int& tm, int& tn) const {
@@ -71,7 +72,8 @@ struct WorkSched {
 //   tail_mode 0: whole tiles only (the last wave may be partial);
 //   tail_mode 1: the tiles of the last partial wave split evenly over the clusters
 //                (>= min_seg k-blocks per segment, <= 4 segments per tile);
-//   tail_mode 2: the tail tiles split in exact halves (needs 2*tail <= nc).
+//   tail_mode 2: the tail tiles split in exact halves (needs 2*tail <= nc);
+//   tail_mode 3: the same halves, both added into C by TMA reduce-add (no partial slabs).
 inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, int nc, int tail_mode, int min_seg = 4) {
   WorkSched s;
   s.tiles_m = tiles_m;
@@ -84,13 +86,15 @@ inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, 
   const int64_t tail = T - (int64_t)s.W * s.nc;
   s.TI = tail * num_kb;
   s.land = 0;
-  if (tail == 0 || tail_mode == 0 || (tail_mode == 2 && 2 * tail > s.nc)) {
+  s.red = 0;
+  if (tail == 0 || tail_mode == 0 || (tail_mode >= 2 && 2 * tail > s.nc)) {
     s.W = (int)((T + s.nc - 1) / s.nc);
     s.ntc = 0;
     s.TI = 0;
-  } else if (tail_mode == 2) {
+  } else if (tail_mode >= 2) {
     s.ntc = (int)(2 * tail);  // exact halves: finisher + one contributor per tile
-    s.land = 1;
+    s.land = tail_mode == 2;
+    s.red = tail_mode == 3;
   } else {
     int64_t ntc = s.nc < tail * 4 ? s.nc : tail * 4;
     const int64_t cap = s.TI / (min_seg < 1 ? 1 : min_seg);

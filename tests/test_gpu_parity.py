@@ -159,18 +159,19 @@ def test_tile_seams_f64(mm):
 
 @pytest.mark.parametrize("dt", ["i8", "bf16", "f64"])
 @pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("streamk", ["default", "1", "2"])
+@pytest.mark.parametrize("streamk", ["default", "1", "2", "3"])
 def test_stream_k_split_tiles(mm, dt, cg, streamk):
     """Few tiles, long K: tiles split over several CTAs/clusters (stream-K partials +
-    finisher) — default policy, the general split (1) and the exact-halves split with
-    landing in the operand ring (2) — and a ragged split tail after full waves."""
+    finisher) — default policy, the general split (1), the exact-halves split with
+    landing in the operand ring (2) and the exact halves added into C by TMA reduce-add (3)
+    — and a ragged split tail after full waves."""
     if dt == "f64" and (cg == 2 or streamk != "default"):
         pytest.skip("FP64: no CTA pair; its stream-K is always on")
     if streamk != "default":
         os.environ["MM_STREAMK"] = streamk
     try:
         for (m, n, p) in [(512, 4096, 512), (130, 3000, 260), (2048, 2048, 2304), (1300, 1024, 2600),
-                          (2304, 1024, 2048)]:
+                          (2304, 1024, 2048), (2560, 768, 2560)]:
             A, B = gen(dt, "exact", 41, m, n, p, {"i8": 255, "bf16": 9, "f64": 2049}[dt])
             Cref, D = ref(dt, A, B)
             check(dt, run_gpu(mm, A, B, dt, cg if dt != "f64" else None), Cref, D, exact=True)
@@ -182,7 +183,7 @@ def test_stream_k_split_tiles(mm, dt, cg, streamk):
 
 
 @pytest.mark.parametrize("dt", ["i8", "bf16"])
-@pytest.mark.parametrize("streamk", ["0", "1"])
+@pytest.mark.parametrize("streamk", ["0", "1", "3"])
 def test_wide_tiles_nt2(mm, dt, streamk):
     """512-wide CTA-pair tiles (two TMEM accumulators), forced on small/ragged shapes,
     with and without the stream-K split tail."""
@@ -198,17 +199,18 @@ def test_wide_tiles_nt2(mm, dt, streamk):
         os.environ.pop("MM_STREAMK", None)
 
 
-@pytest.mark.parametrize("dt", ["f64", "bf16", "i8"])
-def test_split_tile_fixup_repeated(mm, dt):
+@pytest.mark.parametrize("dt,mode", [("f64", "1"), ("bf16", "1"), ("i8", "1"), ("bf16", "3"), ("i8", "3")])
+def test_split_tile_fixup_repeated(mm, dt, mode):
     """Race check of the split-tile fix-up (contributors publish partials, the finisher waits on
-    a counter and adds them): many back-to-back launches of split-heavy shapes, every output
-    compared bit-exactly (exact-integer inputs).  A premature release of the finisher's named
-    barrier (bar.sync by a divergent warp) showed up here as a few wrong rows in one tile."""
-    env = {"f64": {"MM_F64_TILE": "128", "MM_F64_STREAMK": "1"}, "bf16": {"MM_STREAMK": "1"},
-           "i8": {"MM_STREAMK": "1"}}[dt]
+    a counter and adds them; mode 3: one half zeroes C and publishes, both reduce-add into C):
+    many back-to-back launches of split-heavy shapes, every output compared bit-exactly
+    (exact-integer inputs).  A premature release of the finisher's named barrier (bar.sync by a
+    divergent warp) showed up here as a few wrong rows in one tile."""
+    env = {"f64": {"MM_F64_TILE": "128", "MM_F64_STREAMK": "1"}, "bf16": {"MM_STREAMK": mode},
+           "i8": {"MM_STREAMK": mode}}[dt]
     os.environ.update(env)
     try:
-        for (m, n, p) in [(1100, 768, 1700), (513, 2048, 700)]:
+        for (m, n, p) in [(1100, 768, 1700), (513, 2048, 700), (2560, 768, 2560)]:
             A, B = gen(dt, "exact", 49, m, n, p, {"i8": 255, "bf16": 9, "f64": 2049}[dt])
             Cref, _ = ref(dt, A, B)
             Ad, Bd = to_dev(A, dt), to_dev(B, dt)
@@ -219,6 +221,40 @@ def test_split_tile_fixup_repeated(mm, dt):
     finally:
         for k in env:
             os.environ.pop(k, None)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "i8"])
+def test_reduce_add_tail(mm, dt):
+    """Tail tiles split in exact K halves, both added into C by TMA reduce-add (the half holding
+    k-block 0 zeroes C first): C3-like 256-tile shapes whose last wave has <= 37 tiles.  Random
+    inputs: within tolerance of the oracle and bit-identical over repeated launches (two addends
+    into +0 commute exactly); a guard-banded C (no store outside it); int8 wrap-around sums."""
+    os.environ["MM_STREAMK"] = "3"
+    try:
+        for (m, n, p) in [(4096, 512, 4096), (2560, 768, 2560), (2400, 1000, 2700)]:
+            A, B = gen(dt, "random", 51, m, n, p)
+            Cref, D = ref(dt, A, B)
+            Ad, Bd = to_dev(A, dt), to_dev(B, dt)
+            outs = [mm.gemm(Ad, Bd) for _ in range(8)]
+            mm.sync_check()
+            check(dt, outs[0].cpu().numpy(), Cref, D, exact=False)
+            for C in outs[1:]:
+                assert torch.equal(C, outs[0]), (m, n, p)
+        out = torch.float32 if dt == "bf16" else torch.int32
+        m, n, p = 2560, 768, 2560
+        A, B = gen(dt, "exact", 52, m, n, p, 255 if dt == "i8" else 9)
+        Cref, _ = ref(dt, A, B)
+        guard = 8192
+        buf = torch.full((guard + m * p + guard,), -7, dtype=out, device="cuda")
+        C = buf[guard:guard + m * p].view(m, p)
+        C.fill_(123)  # stale contents: the zeroing half must overwrite them
+        mm.gemm(to_dev(A, dt), to_dev(B, dt), out=C)
+        mm.sync_check()
+        h = buf.cpu().numpy()
+        assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7)
+        assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64))
+    finally:
+        os.environ.pop("MM_STREAMK", None)
 
 
 @pytest.mark.parametrize("tile", ["32ks4", "32ks2", "32ks1", "64", "128"])
