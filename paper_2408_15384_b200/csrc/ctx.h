@@ -18,6 +18,7 @@ struct mm_ctx {
   int cc_major = 0, cc_minor = 0;
   void* user_ws = nullptr;
   size_t user_ws_bytes = 0;
+  int c_remote = 0;  // set around products whose C is a peer GPU's memory (fused row-block gather)
   void* ws = nullptr;  // internal, grow-only (padding path)
   size_t ws_bytes = 0;
   int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..2] wave-barrier counters

@@ -704,7 +704,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   int max_cl = 0;
   cudaError_t e = launch_cfg<I8, CG, NT, MC, KA>(cfg, attr, num_sms, &max_cl);
   if (e != cudaSuccess) return e;
-  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA, a.c_tma != 0);
+  const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA, a.c_tma != 0 && !a.no_reduce);
   cfg.gridDim = dim3(sched.nc * CG * MC, 1, 1);
   cfg.stream = s;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, a, sched);

@@ -24,6 +24,7 @@ struct GemmArgs {
   void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
+  int no_reduce;    // tcgen05 kernel: no TMA reduce-add into C (C in a peer GPU's memory)
   int l2_hint;      // tcgen05 kernel: TMA loads of A evict_last, of B evict_first
   unsigned long long* trace;  // optional per-CTA wait-time counters (16 per CTA), MM_TRACE=1
   int debug;        // diagnostics only (MM_DEBUG): bit 0 = tcgen05 producer skips the operand loads

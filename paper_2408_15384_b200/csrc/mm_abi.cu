@@ -214,6 +214,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ws = nullptr;
   a.flags = nullptr;
   a.c_tma = 0;
+  a.no_reduce = ctx->c_remote;
   // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;

@@ -254,6 +254,12 @@ static mm_status row_block(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtyp
     if (st != MM_OK) return st;
     target = full + mine.start * p * eo;
   }
+  // products into a peer's memory: plain TMA stores only (no reduce-add split tail over NVLink)
+  struct RemoteC {
+    mm_ctx* c;
+    RemoteC(mm_ctx* c_, bool on) : c(c_) { c->c_remote = on ? 1 : 0; }
+    ~RemoteC() { c->c_remote = 0; }
+  } remote_c(ctx, (flags & MM_GATHER_C_FUSED) != 0);
 
   if (flags & MM_BCAST_B) {
     // B broadcast in column panels, double-buffered on a communication stream, so the
