@@ -156,9 +156,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* err = args.err;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    if (args.c_tma) tma_prefetch_desc(&tmC);
+    if (!(args.debug & 16)) {  // (diagnostics: bit 4 skips the descriptor prefetch)
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      if (args.c_tma) tma_prefetch_desc(&tmC);
+    }
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), MC);  // one commit from the leader of every pair reading this slot
@@ -645,10 +647,12 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // the first half while its MMAs run) with TMA reduce-add stores — no partial slabs, no
   // read-back, neither half waits for the other's MMAs.
   // Reduce-add stores take ~1.5x as long as plain ones and the zeroing half stores the tile twice,
-  // so int8 (half-length tiles) gains only with long K (C3: 16 k-blocks, neutral; 2560^3 -7 %),
-  // bf16 from 4 k-blocks on (4096^3 +4 %, 2560^3 +5 % over landing, tools/ab_gpu.py).
+  // so int8 (half-length tiles) gains only with long K (C3 K=4096: neutral; 2560^3 -7 %),
+  // bf16 4096^3 +4 %, 2560^3 +5 % over landing (tools/ab_gpu.py).
   int mode = 0;
-  if (tail > 0 && mc == 1 && 2 * tail <= nc && num_kb >= (i8 ? 24 : 4))
+  // (the zeroing and the slower reduce-add read-out cost a few us: the saved half tile must be
+  // longer — K >= 1536 (BF16) / 6144 (INT8); a single 256^3 tile split in halves ran 8.2 -> 10.8 us)
+  if (tail > 0 && mc == 1 && 2 * tail <= nc && K >= (i8 ? 6144 : 1536))
     mode = c_tma ? 3 : ((!i8 && nt == 1 && num_kb >= 8) ? 2 : 0);
   if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
