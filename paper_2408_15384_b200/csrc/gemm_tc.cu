@@ -156,11 +156,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* err = args.err;
 
   if (warp == 0 && lane == 0) {
-    if (!(args.debug & 16)) {  // (diagnostics: bit 4 skips the descriptor prefetch)
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmB);
-      if (args.c_tma) tma_prefetch_desc(&tmC);
-    }
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (args.c_tma) tma_prefetch_desc(&tmC);
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), MC);  // one commit from the leader of every pair reading this slot
