@@ -440,6 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool red_item = sched.red && !(kb0 == 0 && kb1 == num_kb);
       unsigned* red_flag = args.flags + (size_t)t * (CG * MC) + crank;
       if (red_item && kb0 == 0) {
+        // these stores do not follow any load: wait for the previous kernel in the stream (PDL) here,
+        // or they could land before that kernel's own stores to the same C
+        pdl_wait();
         const int64_t zrow = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + q * 32;
         if (n_stores >= 1) {
           if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the buffer

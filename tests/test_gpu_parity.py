@@ -257,6 +257,33 @@ def test_reduce_add_tail(mm, dt):
         os.environ.pop("MM_STREAMK", None)
 
 
+@pytest.mark.parametrize("dt", ["bf16", "i8"])
+def test_reduce_add_tail_same_output_back_to_back(mm, dt):
+    """The reduce-add tail zeroes C before its MMAs finish; with programmatic dependent launch the
+    next product in the stream starts while the previous one still stores.  Back-to-back products
+    into the SAME output, alternating inputs, on shapes whose split tile is a CTA's first item
+    (no full wave): each result must be exactly its own product."""
+    os.environ["MM_STREAMK"] = "3"
+    try:
+        for (m, n, p) in [(1024, 2048, 1024), (512, 4096, 768)]:
+            out = torch.float32 if dt == "bf16" else torch.int32
+            pairs = [gen(dt, "exact", 60 + s, m, n, p, 255 if dt == "i8" else 9) for s in range(2)]
+            refs = [np.asarray(ref(dt, A, B)[0], np.float64) for A, B in pairs]
+            dev = [(to_dev(A, dt), to_dev(B, dt)) for A, B in pairs]
+            C = torch.empty(m, p, dtype=out, device="cuda")
+            snaps = []
+            for it in range(16):
+                Ad, Bd = dev[it % 2]
+                mm.gemm(Ad, Bd, out=C)
+                if it >= 14:
+                    snaps.append(C.clone())
+            mm.sync_check()
+            for it, S in zip((14, 15), snaps):
+                assert np.array_equal(S.cpu().numpy().astype(np.float64), refs[it % 2]), (m, n, p, it)
+    finally:
+        os.environ.pop("MM_STREAMK", None)
+
+
 @pytest.mark.parametrize("tile", ["32ks4", "32ks2", "32ks1", "64", "128"])
 @pytest.mark.parametrize("streamk", ["0", "1"])
 def test_f64_tiles_and_schedules(mm, tile, streamk):
