@@ -5,23 +5,32 @@
 // The operation is PAPER.md:56-60 (§III); A m×n and B n×p are row-major
 // (PAPER.md:87).  What the paper does on a CPU with cache tiling
 // and row-parallel threads is done here as:
-//   * tiles of C (128·CG × 256) walked by a persistent grid of CTA clusters,
-//     grouped along M so concurrently running tiles share B panels in L2;
+//   * tiles of C (128·CG × 256·NT) walked by a persistent grid of CTA clusters
+//     in grouped-raster waves (sched.cuh); above 96 MB of operands a wave
+//     barrier keeps the k-phase of a wave aligned so its tiles share A/B slabs
+//     in L2;
 //   * K-slabs of A (K-major) and B (row-major = N-major, consumed as an
 //     MN-major UMMA operand, so B's "columns" need no transpose)
-//     staged by TMA into 128-byte-swizzled shared memory, STAGES deep,
-//     full/empty mbarriers between the producer warp and the MMA warp;
-//   * one thread issues tcgen05.mma into a TMEM accumulator; two accumulators
-//     (2 × 256 columns = all 512) let the epilogue of tile j overlap the
-//     mainloop of tile j+1;
+//     staged by TMA into 128-byte-swizzled shared memory (KA swizzle atoms of
+//     K per stage), full/empty mbarriers between the producer warp and the MMA
+//     warp;
+//   * one thread issues tcgen05.mma into TMEM: NT = 1, two 256-column
+//     accumulators (the epilogue of tile j overlaps the mainloop of tile j+1);
+//     NT = 2, one 512-column accumulator of two regions released one by one;
 //   * CG = 2: a CTA pair (cluster of 2) runs one M=256 MMA; each CTA stages
-//     its own 128 rows of A and half of B's 256 columns (halving smem traffic
-//     per SM); the leader issues, commits multicast to both.
+//     its own 128 rows of A and half of B's columns; the leader issues and
+//     commits to both.  MC = 2 (knob): two pairs share B slabs by multicast;
+//   * epilogue: tcgen05.ld -> registers -> 128B-swizzled staging -> TMA store;
+//     a split last wave (sched.cuh modes) either adds partial slabs in a fixed
+//     order or, by default, adds exact K halves into C with TMA reduce-add;
 //   * edges (ragged m, n, p): TMA zero-fills out-of-bounds boxes (zeros add
-//     exactly 0 to every sum); stores are predicated per element.
+//     exactly 0 to every sum) and clips out-of-bounds stores.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
-// MMA issuer, warps 2..5 = epilogue (TMEM -> registers -> global).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
+// MMA issuer, warps 2..9 = epilogue (two per TMEM lane quarter).
+// Programmatic dependent launch: everything before the producer's
+// griddepcontrol.wait (and the zeroing of a reduce-add tail) may overlap the
+// previous kernel in the stream.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
