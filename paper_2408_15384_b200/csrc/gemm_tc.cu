@@ -28,9 +28,9 @@
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // MMA issuer, warps 2..9 = epilogue (two per TMEM lane quarter).
-// Programmatic dependent launch: everything before the producer's
-// griddepcontrol.wait (and the zeroing of a reduce-add tail) may overlap the
-// previous kernel in the stream.
+// Programmatic dependent launch: only the prologue overlaps the previous kernel
+// in the stream; griddepcontrol.wait precedes every global access (the producer
+// before its first load, the epilogue warps before zeroing a reduce-add tail).
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
