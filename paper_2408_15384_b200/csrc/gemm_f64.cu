@@ -5,7 +5,7 @@
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) with register accumulators; the
 // operand pipeline is still Blackwell-native: TMA 2-D boxes into a
 // 128-byte-swizzled shared-memory ring with full/empty mbarriers between one
-// producer warp and eight consumer warps ("cache tiling",
+// producer warp and the consumer warps ("cache tiling",
 // PAPER.md:366-373 prefetching/pipelining, done by TMA instead of the CPU).
 //
 // Work split (sched.cuh): whole tiles in grouped-raster waves over the persistent
@@ -20,7 +20,8 @@
 // CTA tile BM×BN (128×128; 64×64 or 32×32 for small problems, where 32×32 tiles
 // give every CTA one whole tile and no fix-up: C1 = 64 tiles), K slab 16 (one
 // 128-B swizzle row of A).  WM×WN consumer warps, each owning a (BM/WM)×(BN/WN)
-// sub-tile.
+// sub-tile: 16 warps (4 per SM sub-partition) at 128×128 and 64×64, so a warp
+// stalled at a k-block boundary leaves three to keep the DMMA pipe busy.
 // Fragment loads are conflict-free with the swizzle because each DMMA's four
 // k indices are taken from rows {b, b+1, b+4, b+5} of the slab (b ∈ {0,2,8,10}):
 // the same four k's for A and B, so each DMMA still adds A[i][k]·B[k][j] over
