@@ -688,6 +688,30 @@ def test_config3_bf16_16384_exact_pins(mm, K):
     assert np.array_equal(C[rows].astype(np.float64), Cr)
 
 
+def test_config4_fp64_32768_exact_pin(mm):
+    """configs[4]'s shape (FP64 32768^3, seed 4) on exact-integer inputs
+    from [-1024, 1024] (every partial sum an integer < 2^53, so exact in any order): the
+    full output's checksum equals the oracle's (tests/golden/oracle_fullsize.json, written by
+    tools/make_golden.py from oracle/ only), bit for bit, as do its corners."""
+    key = "C5x"
+    if key not in FULL:
+        pytest.skip(f"{key} golden not generated yet (tools/make_golden.py --only C5x)")
+    from synthgen import gpu as sgg
+    N = 32768
+    A = sgg.exact_f64(4, sg.ROLE_A, 2049, N, N)
+    B = sgg.exact_f64(4, sg.ROLE_B, 2049, N, N)
+    C = mm.gemm(A, B)
+    mm.sync_check()
+    del A, B
+    torch.cuda.empty_cache()
+    Ch = C.cpu().numpy()
+    del C
+    g = FULL[key]
+    assert Ch[0, 0] == g["C00"] and Ch[0, -1] == g["C0_last"]
+    assert Ch[-1, 0] == g["Clast_0"] and Ch[-1, -1] == g["Clast_last"]
+    assert sg.checksum(Ch) == int(g["checksum"], 16)
+
+
 def test_config4_fp64_32768_sampled(mm):
     """configs[4] at full size on one GPU (the SUMMA G=1 reference), oracle on sampled rows/cols."""
     N = 32768
