@@ -12,7 +12,7 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 A = torch.randn(N, N).to(torch.bfloat16).pin_memory()
 B = torch.randn(N, N).to(torch.bfloat16).pin_memory()
 C = torch.empty(N, N, dtype=torch.float32).pin_memory()
-for blocks in (1, 2, 4, 8, 16):
+for blocks in [int(x) for x in os.environ.get("BLOCKS", "1,2,4,8,16").split(",")]:
     os.environ["MM_HOST_BLOCKS"] = str(blocks)
     mm.gemm_host(A, B, out=C)
     ts = []
