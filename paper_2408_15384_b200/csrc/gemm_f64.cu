@@ -391,9 +391,18 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   // no fix-up: C1 = 64 tiles); else 64x64 (measured: 512^3 20.5 us at 64x64 split vs 26.6 us
   // at 32x32 split).
   pl.bm = pl.bn = 5 * tiles(128) >= 3 * num_sms ? 128 : (tiles(32) <= num_sms ? 32 : 64);
-  if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 128
+  // 96x128 tiles when they fill the last wave almost exactly and 128x128 ones leave it at most
+  // 3/4 full (few waves only: the 24x32 warp tiles are a little less efficient): C2 2000x1500x1750
+  // = 294 tiles (1.99 waves) instead of 224 (1.51) -> 335.9 -> 326.7 us (tools/probe83.sh)
+  if (pl.bm == 128) {
+    const int64_t t96 = ((M + 95) / 96) * ((N + 127) / 128), t128 = tiles(128);
+    auto fill = [&](int64_t T) { const int64_t r = T % num_sms; return r == 0 ? 1.0 : (double)r / num_sms; };
+    if (t96 <= 4 * (int64_t)num_sms && fill(t96) >= 0.9 && fill(t128) <= 0.75) pl.bm = 96;
+  }
+  if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 96 (x128) | 128
     const int v = atoi(e);
     if (v == 32 || v == 64 || v == 128) pl.bm = pl.bn = v;
+    if (v == 96) { pl.bm = 96; pl.bn = 128; }
   }
   const int tiles_m = (int)((M + pl.bm - 1) / pl.bm);
   const int tiles_n = (int)((N + pl.bn - 1) / pl.bn);
@@ -436,6 +445,7 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
 
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                             const CUtensorMap& tmB3, const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
+  if (pl.bm == 96) return launch_impl<96, 128, 4, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
   if (pl.bm == 128) {
     // 16 consumer warps of 32x32 (4 per SM sub-partition, ~96 registers): a warp stalled at a k-block
     // boundary or on a fragment load leaves three others to keep the DMMA pipe busy.  8 warps of

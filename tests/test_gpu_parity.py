@@ -284,12 +284,12 @@ def test_reduce_add_tail_same_output_back_to_back(mm, dt):
         os.environ.pop("MM_STREAMK", None)
 
 
-@pytest.mark.parametrize("tile", ["32ks4", "32ks2", "32ks1", "64", "128"])
+@pytest.mark.parametrize("tile", ["32ks4", "32ks2", "32ks1", "64", "96", "128"])
 @pytest.mark.parametrize("streamk", ["0", "1"])
 def test_f64_tiles_and_schedules(mm, tile, streamk):
     """FP64 kernel at every CTA tile (32x32 with 4 k-block groups of one warp, 2 of 4 warps, or one
     group of 4; 64x64 /
-    128x128 with 8 warps), with whole-tile waves only or with the split last wave, on ragged
+    96x128 and 128x128 with 16 warps), with whole-tile waves only or with the split last wave, on ragged
     and multi-wave shapes; the exact-integer inputs make every tile, seam, k-group and
     partial-tile sum bit-exact."""
     os.environ["MM_F64_TILE"] = tile[:2] if tile.startswith("32") else tile
