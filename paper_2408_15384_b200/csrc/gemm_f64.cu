@@ -430,7 +430,9 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   // 32x32 whole tiles: 4 k-blocks per TMA load (the caller drops to 1 unless n, p are 16-multiples)
   pl.kb = (pl.bm == 32 && mode == 0 && (pl.ks == 1 || pl.ks == 2)) ? 4 : 1;
   if (const char* e = knob("MM_F64_KB")) pl.kb = (pl.kb == 4 && atoi(e) == 4) ? 4 : 1;  // tuning knob
-  pl.sched = sched_build(tiles_m, tiles_n, 8, num_kb, (int)std::max<int64_t>(1, nc), mode);
+  int group_m = 8;
+  if (const char* e = knob("MM_F64_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
+  pl.sched = sched_build(tiles_m, tiles_n, group_m, num_kb, (int)std::max<int64_t>(1, nc), mode);
   pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
   pl.flag_count = (int)T;
   return pl;
