@@ -107,3 +107,43 @@ def test_fuzz_exact(mm, case):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+def _cases_random():
+    rng = random.Random(20261020)
+    out = []
+    for i in range(24):
+        dt = rng.choice(["bf16", "f64"])
+        m, n, p = _dim(rng), _dim(rng), _dim(rng)
+        knobs = KNOBS_F64 if dt == "f64" else KNOBS_TC
+        env = {k: rng.choice(v) for k, v in knobs.items()}
+        out.append((i, dt, m, n, p, {k: v for k, v in env.items() if v is not None}))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases_random(), ids=lambda c: f"r{c[0]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}")
+def test_fuzz_random_values(mm, case):
+    """Random-valued inputs (U[-1,1) FP64, N(0,1) BF16) under random knobs: normalised error
+    within the contract (1e-12 FP64, 2e-2 BF16) and the BF16 diagnostic bound (1e-4)."""
+    i, dt, m, n, p, env = case
+    if dt == "f64":
+        A, B = sg.uniform_f64(800 + i, 1, m, n), sg.uniform_f64(800 + i, 2, n, p)
+        Cref, D = oracle.gemm_f64(A, B), oracle.absden_f64(A, B)
+        tol = 1e-12
+    else:
+        A, B = sg.normal_bf16(800 + i, 1, m, n), sg.normal_bf16(800 + i, 2, n, p)
+        Cref, D = oracle.gemm_bf16(A, B)
+        tol = 1e-4
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        C = mm.gemm(_dev(A, dt), _dev(B, dt))
+        mm.sync_check()
+        err = oracle.normalized_error(C.cpu().numpy(), Cref, D)
+        assert err <= tol, (err, env)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
