@@ -664,9 +664,10 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // bf16 4096^3 +4 %, 2560^3 +5 % over landing (tools/ab_gpu.py).
   int mode = 0;
   // (the zeroing and the slower reduce-add read-out cost a few us: the saved half tile must be
-  // longer — K >= 1536 (BF16) / 4608 (INT8: 4096 neutral, 5120 +2 %, 5632 +5 %); a single 256^3
-  // tile split in halves ran 8.2 -> 10.8 us)
-  if (tail > 0 && mc == 1 && 2 * tail <= nc && K >= (i8 ? 4608 : 1536))
+  // longer — K >= 2304 (BF16: 1536 -4..-6 %, 2048 0..-4 %, 2304 +5.5 %, 3072 +9.5 %) / 4608
+  // (INT8: 4096 neutral, 5120 +2 %, 5632 +5 %); a single 256^3 tile split in halves ran
+  // 8.2 -> 10.8 us)
+  if (tail > 0 && mc == 1 && 2 * tail <= nc && K >= (i8 ? 4608 : 2304))
     mode = c_tma ? 3 : ((!i8 && nt == 1 && num_kb >= 8) ? 2 : 0);
   if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
