@@ -22,7 +22,7 @@ NVFLAGS := -std=c++17 -O3 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvis
            -Iinclude -Ipaper_2408_15384_b200/csrc $(if $(NCCL_INC),-I$(NCCL_INC)) \
            --expt-relaxed-constexpr -diag-suppress 177 -Xptxas -v
 
-.PHONY: all host clean
+.PHONY: all host clean diag
 all: $(SG_LIB) $(OR_LIB) $(MM_LIB)
 host: $(SG_LIB) $(OR_LIB)
 
@@ -34,12 +34,24 @@ $(OR_LIB): oracle/mmref.c
 
 $(MM_LIB): $(MM_SRCS) $(MM_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(MM_SRCS) -ldl 2> paper_2408_15384_b200/build.log || (cat paper_2408_15384_b200/build.log; exit 1)
-	@grep -E "registers|spill|error" paper_2408_15384_b200/build.log | head -40 || true
+	@grep -E "[1-9][0-9]* bytes spill|error" paper_2408_15384_b200/build.log | head -10 || true
+
+# diagnostic build: MM_DEBUG / MM_TRACE / MM_HOST_TRACE knobs (select with MM_B200_LIB=<path>)
+MM_DIAG_LIB := paper_2408_15384_b200/libmm_b200_diag.so
+diag: $(MM_DIAG_LIB)
+$(MM_DIAG_LIB): $(MM_SRCS) $(MM_HDRS)
+	$(NVCC) $(NVFLAGS) -DMM_DIAG -shared -o $@ $(MM_SRCS) -ldl 2> paper_2408_15384_b200/build_diag.log || (cat paper_2408_15384_b200/build_diag.log; exit 1)
 
 clean:
-	rm -f $(SG_LIB) $(OR_LIB) $(MM_LIB)
+	rm -f $(SG_LIB) $(OR_LIB) $(MM_LIB) $(MM_DIAG_LIB)
 
 SGC_LIB := synthgen/libsynthgen_cuda.so
 all: $(SGC_LIB)
 $(SGC_LIB): synthgen/synthgen_cuda.cu
 	$(NVCC) -std=c++17 -O3 $(GENCODE) -fmad=false -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -o $@ $<
+
+# test-only helper (tests/test_gpu_hazards.py): a kernel that holds SMs
+HOG_LIB := tests/libhog.so
+all: $(HOG_LIB)
+$(HOG_LIB): tests/csrc/hog.cu
+	$(NVCC) -std=c++17 -O2 $(GENCODE) -Xcompiler -fPIC -shared -o $@ $<

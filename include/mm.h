@@ -136,6 +136,17 @@ mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
                           const void* A_local, void* B_local, void* C_local, void* C_full,
                           unsigned flags, int root, void* nccl_comm, void* stream);
 
+/* CUDA-IPC export / open of device memory (the peer mapping behind MM_GATHER_C_FUSED, exposed
+ * so a handle can travel by any channel).  mm_ipc_export fills *out with a handle to the
+ * allocation holding dev_ptr plus dev_ptr's offset in it (MM_ERR_USAGE if dev_ptr is not device
+ * memory).  mm_ipc_open, in ANOTHER process, maps it (cached per context; unmapped by mm_destroy)
+ * and returns the address of dev_ptr in this process; products may then store into it (TMA stores
+ * through the mapping — over NVLink when it is a peer GPU's memory).  MM_ERR_RUNTIME if the
+ * handle cannot be opened (e.g. an allocation of this same process). */
+typedef struct { unsigned char bytes[72]; } mm_ipc_handle;
+mm_status mm_ipc_export(mm_ctx* ctx, const void* dev_ptr, mm_ipc_handle* out);
+mm_status mm_ipc_open(mm_ctx* ctx, const mm_ipc_handle* handle, void** dev_ptr);
+
 /* Contiguous block partition of `total` items over G parts:
  * part r gets [start, start+count); the first parts get ⌈total/G⌉, the
  * last non-empty part is short, surplus parts (G > total) are empty. */
@@ -148,6 +159,84 @@ void mm_shard_range(int64_t total, int G, int r, int64_t* start, int64_t* count)
  * Pure host logic (tested without a GPU). */
 int mm_summa_panels(int64_t n, int grid_rows, int grid_cols, int64_t panel, int cap,
                     int64_t* k0, int64_t* kw, int* a_col, int* b_row);
+
+/* ------------------------------------------------------------------ sharded schedule as data
+ * mm_gemm_sharded runs a per-rank PLAN: a list of steps (local products, pitched copies, NCCL
+ * collectives, stream events) that mm_shard_plan computes from the collective's arguments alone
+ * (pure host logic, no device, no communicator).  The same plan can be executed by another runtime
+ * (the test suite runs it over torch.distributed/gloo on CPU with the oracle as the local product,
+ * at world sizes 2-8), so the partition, offsets, pitches, roots and ordering that the GPU path
+ * uses are checked on any machine.  The rules are the ones documented for mm_gemm_sharded above
+ * (PAPER.md:119 row partition; PAPER.md:135 SUMMA / 2.5D).
+ *
+ * Buffers (mm_plan_buf): the caller's A_local, B_local, C_local, C_full (root only), the root's
+ * C_full as mapped into this rank (CPEER, fused gather), and staging buffers S0..S3 of
+ * info.stage_bytes[i] bytes owned by the executor.  Offsets are in bytes.
+ * Streams: 0 = the caller's (compute) stream, 1 = the executor's communication stream.
+ * Communicators (mm_plan_comm): WORLD, and the ROW / COL / DEPTH sub-communicators obtained by
+ * splitting WORLD with info.color[c] / info.key[c] (ncclCommSplit semantics: ranks with equal
+ * colour form one communicator, ordered by key); `peer` is a rank inside the step's communicator.
+ *
+ *   MM_OP_GEMM        C[dst]+dst_off (ld dst_ld elements) (+)= A[src]+src_off (ld src_ld) ·
+ *                     B[src2]+src2_off (ld src2_ld); m×n · n×p; beta 0 overwrite, 1 accumulate;
+ *                     overlap = 1: communication runs concurrently (the product leaves SMs free).
+ *   MM_OP_COPY2D      m rows of n bytes: dst+dst_off (pitch dst_ld bytes) <- src+src_off (pitch src_ld).
+ *   MM_OP_BCAST       n bytes at dst+dst_off, from `peer` to all ranks of `comm` (in place).
+ *   MM_OP_SEND/RECV   n bytes at src+src_off to / dst+dst_off from `peer` of `comm`.
+ *   MM_OP_GROUP_START / MM_OP_GROUP_END   bracket sends/receives issued together.
+ *   MM_OP_REDUCE_SUM  n elements (FP64) at dst+dst_off summed onto `peer` of `comm` (in place).
+ *   MM_OP_MEMSET0     n bytes at dst+dst_off set to zero.
+ *   MM_OP_BARRIER     all ranks of `comm` (device-side: an all-reduce of one word).
+ *   MM_OP_MAP_PEER    collective on WORLD: every rank obtains CPEER = `peer`'s C_full.
+ *   MM_OP_RECORD      record event `event` on `stream`;  MM_OP_WAIT: `stream` waits for `event`.
+ */
+typedef enum {
+  MM_OP_GEMM = 1, MM_OP_COPY2D = 2, MM_OP_BCAST = 3, MM_OP_SEND = 4, MM_OP_RECV = 5, MM_OP_GROUP_START = 6,
+  MM_OP_GROUP_END = 7, MM_OP_REDUCE_SUM = 8, MM_OP_MEMSET0 = 9, MM_OP_BARRIER = 10, MM_OP_MAP_PEER = 11,
+  MM_OP_RECORD = 12, MM_OP_WAIT = 13
+} mm_plan_op;
+typedef enum {
+  MM_BUF_NONE = 0, MM_BUF_A = 1, MM_BUF_B = 2, MM_BUF_C = 3, MM_BUF_CFULL = 4, MM_BUF_CPEER = 5,
+  MM_BUF_S0 = 6, MM_BUF_S1 = 7, MM_BUF_S2 = 8, MM_BUF_S3 = 9
+} mm_plan_buf;
+typedef enum { MM_COMM_WORLD = 0, MM_COMM_ROW = 1, MM_COMM_COL = 2, MM_COMM_DEPTH = 3 } mm_plan_comm;
+
+typedef struct {
+  int32_t op, stream, comm, peer;       /* mm_plan_op; 0/1; mm_plan_comm; rank inside comm */
+  int32_t dst, src, src2, beta;         /* mm_plan_buf ids (GEMM: C = dst, A = src, B = src2) */
+  int64_t dst_off, src_off, src2_off;   /* byte offsets into those buffers */
+  int64_t dst_ld, src_ld, src2_ld;      /* GEMM: leading dimensions in elements; COPY2D: pitches in bytes */
+  int64_t m, n, p;                      /* GEMM: dims; COPY2D: rows = m, row bytes = n; others: n = count */
+  int32_t event, overlap;               /* RECORD/WAIT: event id; GEMM: 1 = overlapped with communication */
+} mm_plan_step;
+
+typedef struct {
+  int32_t steps;           /* steps in the plan (may exceed the cap passed in) */
+  int32_t events;          /* event ids used: [0, events) */
+  int32_t color[4];        /* per mm_plan_comm: split colour of this rank (-1: communicator unused) */
+  int32_t key[4];          /* per mm_plan_comm: rank of this rank inside that communicator */
+  int64_t stage_bytes[4];  /* staging buffers S0..S3 the executor provides */
+} mm_plan_info;
+
+/* The plan rank r of G executes for mm_gemm_sharded(m, n, p, dtype, layout, grid_rows, grid_cols,
+ * flags, root).  `panel`: column-panel width of the B broadcast (row-block) or k-panel width (SUMMA);
+ * 0 = the library default.  Writes at most `cap` steps to `steps` (may be NULL with cap 0) and the
+ * plan's metadata to *info (required).  Returns MM_ERR_USAGE for invalid arguments (the same checks
+ * as mm_gemm_sharded: dims >= 1, 0 <= r < G, root in range, grid consistent with G, flags valid for
+ * the layout; SUMMA layouts for MM_F64 only).  Pure host logic. */
+mm_status mm_shard_plan(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layout layout, int grid_rows,
+                        int grid_cols, unsigned flags, int root, int G, int r, int64_t panel,
+                        mm_plan_step* steps, int cap, mm_plan_info* info);
+
+/* Upper bound, in bytes, of the device memory a context allocates internally for one call with
+ * these arguments: the zero-padded operand copies of the edge path (counted as if
+ * neither A nor B had a 16-byte pitch), the split-tail partial tiles and tickets, and, for G > 1,
+ * the panel staging buffers of the sharded layouts (the largest over all ranks, and for the SUMMA
+ * layouts over every grid that G factors into).  Buffers are allocated lazily, grow only, and are
+ * freed by mm_destroy; a mm_create `workspace` of at least the padding part is used instead of an
+ * internal padding buffer.  Pure host logic: the bound assumes at most 160 SMs.  0 for invalid
+ * arguments. */
+size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layout layout, int G);
 
 /* Number of kernels this context has launched so far (product, padding and
  * fix-up kernels; NCCL's own kernels are not counted). */

@@ -21,7 +21,8 @@ from . import _lib
 from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE, MM_ROW_BLOCK,
                    MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
 
-__all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "MMError", "Context",
+__all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "shard_plan", "workspace_size",
+           "ipc_export", "ipc_open", "MMError", "Context",
            "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
            "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D"]
 
@@ -171,6 +172,68 @@ def summa_panels(n: int, grid_rows: int, grid_cols: int, panel: int):
     bo = (ctypes.c_int * cnt)()
     lib.mm_summa_panels(n, grid_rows, grid_cols, panel, cnt, k0, kw, ao, bo)
     return [(k0[i], kw[i], ao[i], bo[i]) for i in range(cnt)]
+
+
+def shard_plan(m: int, n: int, p: int, dtype: torch.dtype, *, layout: int = MM_ROW_BLOCK,
+               grid: tuple[int, int] = (0, 0), flags: int = 0, root: int = 0, world: int = 1, rank: int = 0,
+               panel: int = 0):
+    """The plan rank `rank` of `world` runs for mm_gemm_sharded (include/mm.h, mm_shard_plan):
+    (steps, info) with steps a list of dicts (op/buffer/communicator names resolved) and info a dict
+    with the communicator split colours/keys and the staging-buffer sizes."""
+    lib = _lib.load()
+    info = _lib.PlanInfo()
+    dt = IN_DTYPE[dtype]
+    st = lib.mm_shard_plan(m, n, p, dt, layout, grid[0], grid[1], flags, root, world, rank, panel, None, 0,
+                           ctypes.byref(info))
+    if st != 0:
+        raise MMError(st, f"mm_shard_plan(m={m}, n={n}, p={p}, layout={layout}, grid={grid}, flags={flags}, "
+                          f"root={root}, world={world}, rank={rank}) rejected the arguments")
+    arr = (_lib.PlanStep * max(1, info.steps))()
+    lib.mm_shard_plan(m, n, p, dt, layout, grid[0], grid[1], flags, root, world, rank, panel, arr, info.steps,
+                      ctypes.byref(info))
+    steps = []
+    for i in range(info.steps):
+        s = arr[i]
+        d = {f: getattr(s, f) for f, _ in _lib.PlanStep._fields_}
+        d["op"] = _lib.OPS[s.op]
+        for b in ("dst", "src", "src2"):
+            d[b] = _lib.BUFS[getattr(s, b)]
+        d["comm"] = _lib.COMMS[s.comm]
+        steps.append(d)
+    meta = {"events": info.events, "color": {_lib.COMMS[c]: info.color[c] for c in range(4)},
+            "key": {_lib.COMMS[c]: info.key[c] for c in range(4)}, "stage_bytes": list(info.stage_bytes)}
+    return steps, meta
+
+
+def workspace_size(m: int, n: int, p: int, dtype: torch.dtype, layout: int = MM_ROW_BLOCK, world: int = 1) -> int:
+    """Upper bound of the device scratch a context allocates for such a call (mm_workspace_size)."""
+    return int(_lib.load().mm_workspace_size(m, n, p, IN_DTYPE[dtype], layout, world))
+
+
+def ipc_export(t: torch.Tensor) -> bytes:
+    """CUDA-IPC handle (72 bytes) of the device memory at t.data_ptr() (mm_ipc_export)."""
+    ctx = context(t.device.index)
+    h = _lib.IpcHandle()
+    ctx.check(_lib.load().mm_ipc_export(ctx.handle, t.data_ptr(), ctypes.byref(h)))
+    return bytes(h.bytes)
+
+
+def ipc_open(handle: bytes, device: int = 0) -> int:
+    """Map another process's exported device memory (mm_ipc_open); returns the device address."""
+    ctx = context(device)
+    h = _lib.IpcHandle()
+    ctypes.memmove(h.bytes, handle, 72)
+    ptr = ctypes.c_void_p()
+    ctx.check(_lib.load().mm_ipc_open(ctx.handle, ctypes.byref(h), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def gemm_ptr(m: int, n: int, p: int, dtype: torch.dtype, A: int, B: int, C: int, device: int = 0,
+             stream: torch.cuda.Stream | None = None):
+    """C = A·B on raw device addresses (e.g. C mapped with ipc_open); async on `stream`."""
+    ctx = context(device)
+    sh = stream.cuda_stream if stream is not None else _raw_stream(device)
+    ctx.check(_lib.load().mm_gemm(ctx.handle, m, n, p, IN_DTYPE[dtype], A, B, C, sh))
 
 
 def _nccl_comm_ptr(group) -> int:

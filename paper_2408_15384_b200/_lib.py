@@ -18,7 +18,32 @@ MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE = 1, 2, 4, 8
 EXPORTS = (
     "mm_create", "mm_destroy", "mm_gemm", "mm_gemm_host", "mm_sync_check", "mm_status_string",
     "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_launches", "mm_version",
+    "mm_shard_plan", "mm_workspace_size", "mm_ipc_export", "mm_ipc_open",
 )
+
+# mm_plan_op / mm_plan_buf / mm_plan_comm (include/mm.h)
+OPS = {1: "GEMM", 2: "COPY2D", 3: "BCAST", 4: "SEND", 5: "RECV", 6: "GROUP_START", 7: "GROUP_END", 8: "REDUCE_SUM",
+       9: "MEMSET0", 10: "BARRIER", 11: "MAP_PEER", 12: "RECORD", 13: "WAIT"}
+BUFS = {0: None, 1: "A", 2: "B", 3: "C", 4: "CFULL", 5: "CPEER", 6: "S0", 7: "S1", 8: "S2", 9: "S3"}
+COMMS = {0: "WORLD", 1: "ROW", 2: "COL", 3: "DEPTH"}
+
+
+class PlanStep(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("stream", ctypes.c_int32), ("comm", ctypes.c_int32), ("peer", ctypes.c_int32),
+                ("dst", ctypes.c_int32), ("src", ctypes.c_int32), ("src2", ctypes.c_int32), ("beta", ctypes.c_int32),
+                ("dst_off", ctypes.c_int64), ("src_off", ctypes.c_int64), ("src2_off", ctypes.c_int64),
+                ("dst_ld", ctypes.c_int64), ("src_ld", ctypes.c_int64), ("src2_ld", ctypes.c_int64),
+                ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("p", ctypes.c_int64),
+                ("event", ctypes.c_int32), ("overlap", ctypes.c_int32)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("events", ctypes.c_int32), ("color", ctypes.c_int32 * 4),
+                ("key", ctypes.c_int32 * 4), ("stage_bytes", ctypes.c_int64 * 4)]
+
+
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 72)]
 
 _i64, _vp, _int, _uint, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_uint, ctypes.c_size_t
 _lib = None
@@ -56,6 +81,15 @@ def load():
     lib.mm_summa_panels.restype = _int
     lib.mm_launches.argtypes = [_vp]
     lib.mm_launches.restype = ctypes.c_uint64
+    lib.mm_shard_plan.argtypes = [_i64, _i64, _i64, _int, _int, _int, _int, _uint, _int, _int, _int, _i64,
+                                  ctypes.POINTER(PlanStep), _int, ctypes.POINTER(PlanInfo)]
+    lib.mm_shard_plan.restype = _int
+    lib.mm_workspace_size.argtypes = [_i64, _i64, _i64, _int, _int, _int]
+    lib.mm_workspace_size.restype = _sz
+    lib.mm_ipc_export.argtypes = [_vp, _vp, ctypes.POINTER(IpcHandle)]
+    lib.mm_ipc_export.restype = _int
+    lib.mm_ipc_open.argtypes = [_vp, ctypes.POINTER(IpcHandle), ctypes.POINTER(_vp)]
+    lib.mm_ipc_open.restype = _int
     lib.mm_version.argtypes = []
     lib.mm_version.restype = ctypes.c_char_p
     _lib = lib

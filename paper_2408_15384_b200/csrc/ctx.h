@@ -19,9 +19,15 @@ struct mm_ctx {
   void* user_ws = nullptr;
   size_t user_ws_bytes = 0;
   int c_remote = 0;  // set around products whose C is a peer GPU's memory (fused row-block gather)
+  int sm_reserve = 0;  // SMs left free for concurrent (communication) kernels, set around overlapped products
+  // cross-stream ordering of the context's scratch (wave counters, split-tile counters and slabs,
+  // padding buffer): a product on a stream other than the previous one waits for the previous one
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t ev_last = nullptr;
+  bool ev_last_valid = false;
   void* ws = nullptr;  // internal, grow-only (padding path)
   size_t ws_bytes = 0;
-  int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..2] wave-barrier counters
+  int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..3] wave-barrier counters + abandoned flag
   int wave_sync = 1;
   // mm_gemm_host staging
   void* hbuf[3] = {nullptr, nullptr, nullptr};
@@ -30,18 +36,23 @@ struct mm_ctx {
   // sharded scratch (panels, gathered rows)
   void* sbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t sbuf_bytes[4] = {0, 0, 0, 0};
-  void* row_comm = nullptr;  // SUMMA sub-communicators (ncclComm_t), cached per parent/grid
-  void* col_comm = nullptr;
-  void* depth_comm = nullptr;  // 2.5D layer communicator
-  int split_layers = 0;
+  // sharded plans: ROW / COL / DEPTH sub-communicators (ncclComm_t, index = mm_plan_comm), cached
+  // per (parent communicator, split colour, key)
+  void* sub_comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  int split_color[4] = {-1, -1, -1, -1}, split_key[4] = {-1, -1, -1, -1};
   void* split_parent = nullptr;
-  int split_rows = 0, split_cols = 0;
+  std::vector<cudaEvent_t> plan_events;  // the plan's event ids
   void* sk_ws = nullptr;  // stream-K partial tiles (both kernels)
   size_t sk_ws_bytes = 0;
   unsigned* sk_flags = nullptr;  // stream-K per-tile counters (self-resetting)
   size_t sk_flag_count = 0;
   void* ipc_xchg = nullptr;  // device staging for the IPC handle exchange (fused gather)
-  std::vector<std::pair<std::string, void*>> ipc_open;  // opened peer allocations (handle bytes -> base)
+  struct IpcMap {
+    std::string handle;  // cudaIpcMemHandle_t bytes
+    void* base;
+    size_t bytes;
+  };
+  std::vector<IpcMap> ipc_open;  // allocations of other processes mapped by mm_ipc_open
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   uint64_t launches = 0;  // kernels launched by this context
@@ -55,6 +66,9 @@ struct mm_ctx {
   int map_cache_used = 0, map_cache_next = 0;
   std::string last_error;
 };
+
+extern "C" void mm_release_comms(mm_ctx* ctx);  // shard.cu: sub-communicators
+extern "C" void mm_release_ipc(mm_ctx* ctx);    // shard.cu: IPC mappings, events, small buffers
 
 namespace mmb {
 
@@ -79,6 +93,8 @@ size_t dtype_out_size(mm_dtype t);
 // grow-only device buffer owned by ctx (synchronizes the device before freeing an old buffer)
 mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need);
 // internal C (+)= A·B with explicit leading dimensions (elements); beta_one only for MM_F64.
+// MM_OK, or MM_ERR_UNSUPPORTED when a diagnostic-only knob is set for the release library.
+mm_status refuse_diag_knobs(mm_ctx* ctx);
 mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s);
 

@@ -12,10 +12,10 @@
 // CTAs (concurrent tiles share A row panels and B column panels in L2), then the
 // tiles of the last, partial wave split "stream-K" style over all CTAs, so every
 // SM gets the same number of DMMA k-blocks (C2: 224 tiles on 148 SMs = 1 wave +
-// an even tail).  A split tile is finished by the CTA holding its k-block 0; the
-// other contributors publish partial tiles to a workspace and bump a per-tile
-// counter; the finisher adds them in CTA order — a fixed order, so results are
-// deterministic run to run.
+// an even tail).  The parts of a split tile take tickets; all but the last to finish
+// publish partial tiles to a workspace, and the last adds them in segment order — a
+// fixed order, so results are run-to-run identical — without any CTA waiting for one
+// that may not be resident yet.
 //
 // CTA tile BM×BN (128×128; 64×64 or 32×32 for small problems, where 32×32 tiles
 // give every CTA one whole tile and no fix-up: C1 = 64 tiles), K slab 16 (one
@@ -64,7 +64,7 @@ struct F64Cfg {
   static constexpr int BOX_STRIDE = KB * BBOX_BYTES;          // between B column boxes of one slot
   static constexpr int SCR_BYTES = (KS - 1) * BM * BN * 8;  // accumulators of groups 1..KS-1
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + 1024;
-  static_assert(STAGES >= 4 && 16 * STAGES <= 1024, "ring");
+  static_assert(STAGES >= 4 && 16 * STAGES <= 1008, "ring (+ the ticket word at the end of the barrier area)");
   static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
   static constexpr int NI = BN / WN / 8;  // 8-col DMMA tiles per warp (even: pairs share a 16-col box)
   static_assert(NI % 2 == 0 && MI >= 1, "warp tile");
@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
   const uint32_t bar0 = smem_u32(smem + STAGES * Cfg::STAGE_BYTES);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  volatile unsigned* tick_slot = reinterpret_cast<volatile unsigned*>(smem + STAGES * Cfg::STAGE_BYTES + 1016);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -284,45 +285,84 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
         unsigned long long* tl; bool on;
         __device__ ~StoreMark() { if (on) tl[5] = globaltimer_ns(); }
       } mark{tl, tl != nullptr && warp == 0 && lane == 0 && j == 0};
-      if (!whole && kb0 != 0) {
-        // ---- contributor: publish the partial tile, then signal the finisher
-        double* slot = part + (size_t)c * (BM * BN);
-#pragma unroll
-        for (int mi = 0; mi < Cfg::MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < Cfg::NI; ++ni) {
-            const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-            st_cg_d2(slot + r * BN + cc, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
-          }
-        __threadfence();
+      if (!whole) {
+        // ---- split tile: segments c_first .. c_last of the tail range hold its k-blocks in order
+        // (c_first from k-block 0).  Each part takes a ticket; every part but the last to finish
+        // publishes its partial tile, and the last one adds them all in segment order (fixed, so
+        // run-to-run identical whoever finishes last).  A CTA only waits for parts that took their
+        // tickets earlier — running CTAs that are just publishing — never for one that may not have
+        // started (the grid need not be co-resident).
+        const int64_t ti0 = (int64_t)(t - sched.W * sched.nc) * num_kb;
+        const int c_first = sched.tail_cluster_of(ti0);
+        const int c_last = sched.tail_cluster_of(ti0 + num_kb - 1);
+        const unsigned nparts = (unsigned)(c_last - c_first + 1);
+        unsigned* tick = args.flags + t;
+        unsigned* pub = args.flags + (size_t)sched.tiles_m * sched.tiles_n + t;
+        // two slots per CTA: its first tail segment (role 0) and its last (role 1, holds k-block 0)
+        auto slot_of = [&](int cc) { return part + ((size_t)cc * 2 + (cc == c_first ? 1 : 0)) * (BM * BN); };
+        if (warp == 0 && lane == 0) *tick_slot = atomic_add_acq_rel_gpu(tick, 1u);
         named_bar(1, NTILE * 32);
-        if (warp == 0 && lane == 0) red_release_gpu_add(args.flags + t, 1u);
-      } else {
-        if (!whole) {
-          // ---- finisher (holds k-block 0): wait for the other contributors, add them in CTA order
-          const int c_last = sched.tail_cluster_of((int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1);
-          const unsigned expect = (unsigned)(c_last - c);
-          if (warp == 0 && lane == 0) {
-            if (!counter_wait(args.flags + t, expect, err, 13)) ok = false;
-            else *(volatile unsigned*)(args.flags + t) = 0u;  // reset for the next launch
-          }
-          // bar.sync is .aligned: warp 0 must reconverge (lane 0 done waiting) before it arrives,
-          // else the barrier can release the other warps before the partials are acquired
-          __syncwarp();
+        const unsigned tk = *tick_slot;
+        named_bar(1, NTILE * 32);
+        if (tk + 1u < nparts) {
+          // ---- not last: publish the partial tile, then count it
+          double* slot = slot_of(c);
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              st_cg_d2(slot + r * BN + cc, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+            }
+          __threadfence();
           named_bar(1, NTILE * 32);
-          for (int q = c + 1; q <= c_last; ++q) {
-            const double* slot = part + (size_t)q * (BM * BN);
-#pragma unroll
-            for (int mi = 0; mi < Cfg::MI; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < Cfg::NI; ++ni) {
-                const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
-                const double2 v = ld_cg_d2(slot + r * BN + cc);
-                acc[mi][ni][0] += v.x;
-                acc[mi][ni][1] += v.y;
-              }
+          if (warp == 0 && lane == 0) red_release_gpu_add(pub, 1u);
+          continue;
+        }
+        // ---- last: wait for the publications (bounded: their CTAs are running), reset the counters
+        if (warp == 0 && lane == 0) {
+          if (!counter_wait(pub, nparts - 1u, err, 13)) {
+            ok = false;
+          } else {
+            *(volatile unsigned*)tick = 0u;
+            *(volatile unsigned*)pub = 0u;
           }
         }
+        // bar.sync is .aligned: warp 0 must reconverge (lane 0 done waiting) before it arrives,
+        // else the barrier can release the other warps before the partials are acquired
+        __syncwarp();
+        named_bar(1, NTILE * 32);
+        // acc := part(c_first) + part(c_first+1) + ... + part(c_last).  When this CTA is not c_first,
+        // its own part goes through its slot too (each thread re-reads only what it stored itself):
+        // the sum then reads every part from the workspace, keeping register pressure at the old level.
+        if (c != c_first) {
+          double* mine = slot_of(c);
+          const double* first = slot_of(c_first);
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              st_cg_d2(mine + r * BN + cc, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+              const double2 v = ld_cg_d2(first + r * BN + cc);
+              acc[mi][ni][0] = v.x;
+              acc[mi][ni][1] = v.y;
+            }
+        }
+        for (int qq = c_first + 1; qq <= c_last; ++qq) {
+          const double* slot = slot_of(qq);
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              const double2 v = ld_cg_d2(slot + r * BN + cc);
+              acc[mi][ni][0] += v.x;
+              acc[mi][ni][1] += v.y;
+            }
+        }
+      }
+      {
         // ---- epilogue: registers -> global (predicated on the ragged edges), β ∈ {0, 1}
 #pragma unroll
         for (int mi = 0; mi < Cfg::MI; ++mi) {
@@ -433,8 +473,9 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   int group_m = 8;
   if (const char* e = knob("MM_F64_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
   pl.sched = sched_build(tiles_m, tiles_n, group_m, num_kb, (int)std::max<int64_t>(1, nc), mode);
-  pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * pl.bm * pl.bn * sizeof(double);
-  pl.flag_count = (int)T;
+  // two partial-tile slots per CTA (its first and its last tail segment); tickets + publish counts
+  pl.ws_bytes = (size_t)std::max(1, pl.sched.ntc) * 2 * pl.bm * pl.bn * sizeof(double);
+  pl.flag_count = (int)(2 * T);
   return pl;
 }
 

@@ -120,6 +120,15 @@ __device__ __forceinline__ void add_words(uint32_t (&v)[32], const uint4 (&w)[8]
 }
 
 template <bool I8>
+__device__ __forceinline__ void add_regs(uint32_t (&v)[32], const uint32_t (&o)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if constexpr (I8) v[i] = (uint32_t)((int32_t)v[i] + (int32_t)o[i]);
+    else v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(o[i]));
+  }
+}
+
+template <bool I8>
 __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict__ src /* = slab + slab_index(c,q,0,l) */) {
   uint4 w[8];
 #pragma unroll
@@ -151,6 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * Cfg::STAGES + 2 + a); };
   auto land_bar = [&](int q) { return bar0 + 8u * (2 * Cfg::STAGES + 4 + q); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + 8 * (2 * Cfg::STAGES + 12));
+  volatile unsigned* tick_slot = reinterpret_cast<volatile unsigned*>(bar_area + 8 * (2 * Cfg::STAGES + 13));
+  static_assert(8 * (2 * Cfg::STAGES + 14) <= 1024, "barrier area");
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -210,10 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; ok && sched.item(cl, j, t, kb0, kb1); ++j) {
         // Wave barrier: start item j only when every CTA has issued all loads of its
         // item j-1, so the tiles of a wave walk K in step and share A/B slabs in L2.
+        // Soft (bounded, abandoned on time-out): no CTA ever depends on another being resident.
         const uint64_t tb0 = args.trace ? globaltimer_ns() : 0;
-        if (args.wave_sync && j > 0 && j <= sched.W &&
-            !counter_wait(args.sync, (unsigned)j * gridDim.x, err, 5))
-          break;
+        if (args.wave_sync && j > 0 && j <= sched.W) soft_wave_wait(args.sync, (unsigned)j * gridDim.x);
         if (args.trace) tr_barrier += globaltimer_ns() - tb0;
         int tm, tn;
         sched.tile_coords(t, tm, tn);
@@ -233,13 +243,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if constexpr (CG == 1) {
             mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
             if (args.l2_hint) {
-              tma_load_2d_hint(sa, &tmA, full_bar(stage), k0, m0, pol_a);
+#pragma unroll
+              for (int a = 0; a < KA; ++a)
+                tma_load_2d_hint(sa + a * Cfg::A_ATOM, &tmA, full_bar(stage), k0 + a * Cfg::BKA, m0, pol_a);
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_hint(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
                                  n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
             } else {
-              tma_load_2d(sa, &tmA, full_bar(stage), k0, m0);
+#pragma unroll
+              for (int a = 0; a < KA; ++a) tma_load_2d(sa + a * Cfg::A_ATOM, &tmA, full_bar(stage), k0 + a * Cfg::BKA, m0);
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
@@ -263,7 +276,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
             if (args.l2_hint) {
-              tma_load_2d_pair_hint(sa, &tmA, leader_full, k0, m0, pol_a);
+#pragma unroll
+              for (int a = 0; a < KA; ++a)
+                tma_load_2d_pair_hint(sa + a * Cfg::A_ATOM, &tmA, leader_full, k0 + a * Cfg::BKA, m0, pol_a);
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_pair_hint(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
@@ -438,20 +453,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mbar_arrive(tempty_bar(a));
       }
     };
+    // Split tiles (sched.cuh): no CTA ever waits for one that may not have started.  Each part
+    // of a split tile takes a ticket (one atomic per CTA, shared with the eight epilogue warps);
+    // only a CTA that holds a ticket waits, and only for parts whose tickets were taken earlier —
+    // CTAs already running whose remaining work (zeroing, or publishing a partial slab) waits on
+    // nothing.  Counters: tickets [0, T·CG·MC), publish counts [T·CG·MC, 2·T·CG·MC).
+    const size_t tcount = (size_t)sched.tiles_m * sched.tiles_n * (CG * MC);
+    auto take_ticket = [&](unsigned* ctr) -> unsigned {
+      if (ew == 0 && lane == 0) *tick_slot = atomic_add_acq_rel_gpu(ctr, 1u);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const unsigned tk = *tick_slot;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      return tk;
+    };
+    // partial slab of cluster cc for a split tile whose first part is held by c_first: each cluster
+    // has at most two split parts (the first and the last segment of its tail range), one slot each
+    auto slab_of = [&](int cc, int c_first) {
+      const size_t role = cc == c_first ? 1 : 0;
+      return reinterpret_cast<uint4*>(part + (((size_t)cc * 2 + role) * (CG * MC) + crank) * (128 * Cfg::TILE_N));
+    };
     int t, kb0, kb1;
     for (int j = 0; sched.item(cl, j, t, kb0, kb1); ++j) {
       int tm, tn;
       sched.tile_coords(t, tm, tn);
       const int acc = j % Cfg::NBUF;
       const uint32_t use = (uint32_t)(j / Cfg::NBUF);
-      // reduce-add tail (sched.red): the half holding k-block 0 zeroes this CTA's rows of the tile in C
-      // while its MMAs run, then publishes that; both halves later add into C with TMA reduce-add
+      // reduce-add tail (sched.red): both halves add into C with TMA reduce-add; the half that takes
+      // the first ticket zeroes this CTA's rows of the tile in C while its MMAs run and publishes it
       const bool red_item = sched.red && !(kb0 == 0 && kb1 == num_kb);
       unsigned* red_flag = args.flags + (size_t)t * (CG * MC) + crank;
-      if (red_item && kb0 == 0) {
-        // these stores do not follow any load: wait for the previous kernel in the stream (PDL) here,
-        // or they could land before that kernel's own stores to the same C
+      bool red_zeroer = false;
+      if (red_item) {
+        // the ticket and the zeros follow no load of this launch: wait for the previous kernel in the
+        // stream (PDL) first, or the zeros could land before that kernel's own stores to the same C
         pdl_wait();
+        red_zeroer = take_ticket(red_flag) == 0u;
+      }
+      if (red_zeroer) {
         const int64_t zrow = (int64_t)tm * Cfg::M_TILE + pair * Cfg::M_MMA + rank * Cfg::BM + q * 32;
         if (n_stores >= 1) {
           if (lane == 0) bulk_wait_read<0>();  // this warp's previous store has read the buffer
@@ -471,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (ew == 0 && lane == 0) {
           asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before the release
-          red_release_gpu_add(red_flag, 1u);
+          red_release_gpu_add(red_flag, 2u);  // ticket (1) + ticket (1) + zeroed (2) = 4
         }
       }
       const uint64_t tq0 = args.trace ? globaltimer_ns() : 0;
@@ -487,10 +525,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row_base = row - lane;  // first row of this warp's 32-row block
       const int64_t col_t = (int64_t)tn * Cfg::TILE_N;
       if (red_item) {
-        if (kb0 != 0) {
-          // wait until the partner half has zeroed these rows (and reset its flag for the next launch)
+        if (!red_zeroer) {
+          // wait until the other half (it took the first ticket, so it is running) has zeroed these
+          // rows, then reset the counter for the next launch
           if (ew == 0 && lane == 0) {
-            if (counter_wait(red_flag, 1u, err, 8)) *(volatile unsigned*)red_flag = 0u;
+            if (counter_wait(red_flag, 4u, err, 8)) *(volatile unsigned*)red_flag = 0u;
             asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired zeros before the reduce-adds
           }
           __syncwarp();
@@ -521,68 +560,94 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
           if (NT == 2 && i + 2 == HCH / 2) release(0);  // region 0 (chunks 0..7) read out: its MMAs may start
         }
-      } else if (kb0 != 0) {
-        // contributor: publish this CTA's 128 x TILE_N partial slab, then signal the finisher
-        uint4* slot = reinterpret_cast<uint4*>(part + ((size_t)tail_c * (CG * MC) + crank) * (128 * Cfg::TILE_N));
-#pragma unroll 1
-        for (int c = h; c < NCH; c += 2) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_row + c * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            st_cg_u4(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
-        }
-        __threadfence();
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (ew == 0 && lane == 0) red_release_gpu_add(args.flags + (size_t)t * (CG * MC) + crank, 1u);
       } else {
-        // finisher (holds k-block 0): wait for the contributors, add their slabs in cluster order
-        const int64_t ti_last = (int64_t)(t - sched.W * sched.nc) * num_kb + num_kb - 1;
-        const int c_last = sched.tail_cluster_of(ti_last);
-        if (ew == 0 && lane == 0) {
-          if (counter_wait(args.flags + (size_t)t * (CG * MC) + crank, (unsigned)(c_last - tail_c), err, 6))
-            *(volatile unsigned*)(args.flags + (size_t)t * (CG * MC) + crank) = 0u;  // reset for the next launch
-        }
-        __syncwarp();  // reconverge warp 0 before the (.aligned) named barrier
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (sched.land && c_last == tail_c + 1) {
-          // Exact-halves split: this is the cluster's last item, so its operand ring is idle
-          // (all loads consumed, all MMAs retired).  Land the partner's slab there with one
-          // 4-KB bulk copy per chunk (all in flight at once), then add it from shared memory.
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(part + ((size_t)c_last * (CG * MC) + crank) * (128 * Cfg::TILE_N));
-          if (lane == 0) {
-            // the slab was written by another SM through the generic proxy and acquired above;
-            // order that before the async-proxy (bulk copy) reads of it
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_arrive_expect_tx(land_bar((int)ew), HCH * 4096u);
-            for (int c = h; c < NCH; c += 2)
-              bulk_copy_g2s(sA + (uint32_t)(c * 4 + q) * 4096u, src + slab_index(c, (int)q, 0, 0) * 16, 4096u,
-                            land_bar((int)ew));
-          }
-          mbar_wait(land_bar((int)ew), 0u, err, 7);
+        // Split tile (modes 1, 2): segments c_first .. c_last of the tail range hold its k-blocks in
+        // order (c_first from k-block 0).  Every part but the last to finish publishes its slab; the
+        // last adds all of them in segment order — the same fixed order whoever finishes last, so
+        // results are run-to-run identical.
+        const int64_t ti0 = (int64_t)(t - sched.W * sched.nc) * num_kb;
+        const int c_first = sched.tail_cluster_of(ti0);
+        const int c_last = sched.tail_cluster_of(ti0 + num_kb - 1);
+        const unsigned nparts = (unsigned)(c_last - c_first + 1);
+        unsigned* tick = args.flags + (size_t)t * (CG * MC) + crank;
+        unsigned* pub = tick + tcount;
+        if (take_ticket(tick) + 1u < nparts) {
+          uint4* slot = slab_of(tail_c, c_first);
 #pragma unroll 1
           for (int c = h; c < NCH; c += 2) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(t_row + c * 32, v);
-            uint4 w[8];
+            tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              w[i] = *reinterpret_cast<const uint4*>(smem + (size_t)(c * 4 + q) * 4096 + i * 512 + lane * 16);
-            tmem_ld_wait();
-            add_words<I8>(v, w);
-            emit(v, row_base, col_t + c * 32);
+              st_cg_u4(slot + slab_index(c, (int)q, i, (int)lane), make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
           }
+          __threadfence();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (ew == 0 && lane == 0) red_release_gpu_add(pub, 1u);
         } else {
+          // last part: the others took their tickets earlier, so they are running and only publishing
+          if (ew == 0 && lane == 0) {
+            if (counter_wait(pub, nparts - 1u, err, 6)) {
+              *(volatile unsigned*)tick = 0u;  // reset both counters for the next launch
+              *(volatile unsigned*)pub = 0u;
+            }
+          }
+          __syncwarp();  // reconverge warp 2 before the (.aligned) named barrier
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (sched.land && nparts == 2u) {
+            // Exact-halves split: this is the cluster's last item, so its operand ring is idle (all
+            // loads consumed, all MMAs retired).  Land the other half's slab there with one 4-KB bulk
+            // copy per chunk (all in flight at once), then add it from shared memory (two FP32 addends
+            // commute exactly, so the order of the halves does not matter).
+            const int other = tail_c == c_first ? c_last : c_first;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(slab_of(other, c_first));
+            if (lane == 0) {
+              // the slab was written by another SM through the generic proxy and acquired above;
+              // order that before the async-proxy (bulk copy) reads of it
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              mbar_arrive_expect_tx(land_bar((int)ew), HCH * 4096u);
+              for (int c = h; c < NCH; c += 2)
+                bulk_copy_g2s(sA + (uint32_t)(c * 4 + q) * 4096u, src + slab_index(c, (int)q, 0, 0) * 16, 4096u,
+                              land_bar((int)ew));
+            }
+            mbar_wait(land_bar((int)ew), 0u, err, 7);
 #pragma unroll 1
-          for (int c = h; c < NCH; c += 2) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_row + c * 32, v);
-            tmem_ld_wait();
-            for (int qq = tail_c + 1; qq <= c_last; ++qq)
-              add32<I8>(v, reinterpret_cast<const uint4*>(part + ((size_t)qq * (CG * MC) + crank) * (128 * Cfg::TILE_N)) +
-                               slab_index(c, (int)q, 0, (int)lane));
-            emit(v, row_base, col_t + c * 32);
+            for (int c = h; c < NCH; c += 2) {
+              uint32_t v[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, v);
+              uint4 w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                w[i] = *reinterpret_cast<const uint4*>(smem + (size_t)(c * 4 + q) * 4096 + i * 512 + lane * 16);
+              tmem_ld_wait();
+              add_words<I8>(v, w);
+              emit(v, row_base, col_t + c * 32);
+            }
+          } else {
+#pragma unroll 1
+            for (int c = h; c < NCH; c += 2) {
+              uint32_t o[32], v[32];
+              tmem_ld_32x32b_x32(t_row + c * 32, o);
+              tmem_ld_wait();
+              // v = part(c_first) + part(c_first+1) + ... + part(c_last), this CTA's own from TMEM
+              if (c_first == tail_c) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = o[i];
+              } else {
+                const uint4* s0 = slab_of(c_first, c_first) + slab_index(c, (int)q, 0, (int)lane);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const uint4 w = ld_cg_u4(s0 + i * 32);
+                  v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+                }
+              }
+              for (int qq = c_first + 1; qq <= c_last; ++qq) {
+                if (qq == tail_c) add_regs<I8>(v, o);
+                else add32<I8>(v, slab_of(qq, c_first) + slab_index(c, (int)q, 0, (int)lane));
+              }
+              emit(v, row_base, col_t + c * 32);
+            }
           }
         }
       }
@@ -617,11 +682,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < 5; ++k) tr[8 + k] = tr_c[k];
     }
   }
-  // the last CTA to finish resets the wave-barrier counters for the next launch
+  // the last CTA to finish resets the wave-barrier counters (and the abandoned flag) for the next launch
   if (args.wave_sync && threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(args.sync + 1, 1u) == gridDim.x - 1) {
       atomicExch(args.sync, 0u);
+      atomicExch(args.sync + 2, 0u);
       atomicExch(args.sync + 1, 0u);
     }
   }
@@ -652,13 +718,13 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // (measured: C4 55 waves +0.6 %, C3 3 waves -12 %; tools/ab_gpu.py).
   // Default: split the tail tiles into exact halves when there are enough clusters
   // (2*tail <= nc) and 256-wide tiles (a 128 x 256 slab fits the idle operand ring of the
-  // finisher, which then lands its partner's slab with bulk copies); MM_STREAMK=1 forces
+  // half that finishes last, which then lands the other's slab with bulk copies); MM_STREAMK=1 forces
   // the general split (partials read from global memory), MM_STREAMK=0 disables both.
   // (bf16 only: int8 tiles are half as long, so the fixed fix-up cost outweighs the saved
   // half tile — measured C3 -3.4 %, bf16 4096^3 +4.1 %, tools/ab_gpu.py)
   // Mode 3 (when C takes TMA stores): the same exact halves, both added into C (zeroed by
-  // the first half while its MMAs run) with TMA reduce-add stores — no partial slabs, no
-  // read-back, neither half waits for the other's MMAs.
+  // the half that takes the first ticket, while its MMAs run) with TMA reduce-add stores —
+  // no partial slabs, no read-back, neither half waits for the other's MMAs.
   // Reduce-add stores take ~1.5x as long as plain ones and the zeroing half stores the tile twice,
   // so int8 (half-length tiles) gains only with long K (C3 K=4096: neutral; 2560^3 -7 %),
   // bf16 4096^3 +4 %, 2560^3 +5 % over landing (tools/ab_gpu.py).
@@ -770,8 +836,9 @@ void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N
   const int mcl = max_clusters_impl(i8, cg, nt, mc, ka, num_sms);
   const WorkSched sc = make_sched(i8, cg, nt, mc, M, N, K, num_sms, mcl, ka, true);
   const WorkSched sc2 = make_sched(i8, cg, nt, mc, M, N, K, num_sms, mcl, ka, false);  // (C without TMA stores)
-  *ws_bytes = (size_t)std::max(sc.ntc, sc2.ntc) * cg * mc * 128 * kBN * nt * 4;
-  *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc;
+  // two partial-slab slots per cluster (its first and its last tail segment), tickets + publish counts
+  *ws_bytes = (size_t)std::max(sc.ntc, sc2.ntc) * 2 * cg * mc * 128 * kBN * nt * 4;
+  *flag_count = (size_t)sc.tiles_m * sc.tiles_n * cg * mc * 2;
 }
 
 cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,

@@ -155,9 +155,70 @@ int force_cg() {
 
 }  // namespace
 
+// Diagnostic knobs (MM_DEBUG skips operand loads or output stores — results are garbage by design;
+// MM_TRACE / MM_HOST_TRACE synchronize the stream to print timelines) exist only in the diagnostic
+// build (`make diag` -> libmm_b200_diag.so, -DMM_DIAG).  The release library refuses them.
+mm_status refuse_diag_knobs(mm_ctx* ctx) {
+#ifndef MM_DIAG
+  for (const char* k : {"MM_DEBUG", "MM_TRACE", "MM_HOST_TRACE"})
+    if (knob(k))
+      return set_err(ctx, MM_ERR_UNSUPPORTED, "%s is a diagnostic knob of the diagnostic build only (make diag, "
+                     "MM_B200_LIB=.../libmm_b200_diag.so); unset it for the release library", k);
+#else
+  (void)ctx;
+#endif
+  return MM_OK;
+}
+
+namespace {
+// The context's scratch (wave-barrier counters, split-tile tickets and slabs, padding buffer) is
+// shared by its launches, so they must not overlap: a product enqueued on a stream other than the
+// previous product's waits for that one first (one event per context).  Inside a CUDA-graph capture
+// the caller owns the ordering (no cross-capture events).
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+mm_status order_after_previous(mm_ctx* ctx, cudaStream_t s, bool cap) {
+  if (cap || !ctx->ev_last_valid || s == ctx->last_stream) return MM_OK;
+  if (cudaStreamWaitEvent(s, ctx->ev_last, 0) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "cross-stream ordering failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return MM_OK;
+}
+mm_status record_launch(mm_ctx* ctx, cudaStream_t s, bool cap) {
+  if (cap) return MM_OK;
+  if (!ctx->ev_last && cudaEventCreateWithFlags(&ctx->ev_last, cudaEventDisableTiming) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "event creation failed");
+  if (cudaEventRecord(ctx->ev_last, s) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "event record failed: %s", cudaGetErrorString(cudaGetLastError()));
+  ctx->last_stream = s;
+  ctx->ev_last_valid = true;
+  return MM_OK;
+}
+}  // namespace
+
+mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
+                       const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s);
+
 mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s) {
+  const bool cap = capturing(s);
+  mm_status st = order_after_previous(ctx, s, cap);
+  if (st != MM_OK) return st;
+  st = gemm_ld_impl(ctx, m, n, p, dtype, A, lda, B, ldb, C, ldc, beta_one, s);
+  if (st != MM_OK) return st;
+  return record_launch(ctx, s, cap);
+}
+
+mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
+                       const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s) {
   const size_t esz = dtype_in_size(dtype);
+  // persistent grids over the SMs not reserved for concurrent (communication) kernels
+  const int num_sms = std::max(4, (ctx->num_sms - std::max(0, ctx->sm_reserve)) & ~1);
   // ---- edge path: operands TMA cannot read in place are copied to a zero-padded pitch.
   const bool padA = !tma_ok(A, lda, esz);
   const bool padB = !tma_ok(B, ldb, esz);
@@ -214,15 +275,24 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
   a.ws = nullptr;
   a.flags = nullptr;
   a.c_tma = 0;
+  // C in another process's (a peer GPU's) memory: plain stores only, no TMA reduce-add split tail
   a.no_reduce = ctx->c_remote;
+  for (const auto& mp : ctx->ipc_open)
+    if (reinterpret_cast<const uint8_t*>(C) >= static_cast<const uint8_t*>(mp.base) &&
+        reinterpret_cast<const uint8_t*>(C) < static_cast<const uint8_t*>(mp.base) + std::max<size_t>(mp.bytes, 1))
+      a.no_reduce = 1;
   // L2 eviction hints on the operand loads: measured no gain (A evict_last) or a loss
   // (B evict_first: C4 DRAM reads 8.9 -> 12.7 GB), so off unless requested.
   a.l2_hint = 0;
   a.trace = nullptr;
   a.debug = 0;
   a.ka = 1;
+#ifdef MM_DIAG
   if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
+#else
+  const bool trace = false;
+#endif
   int trace_nt = 0, trace_mc = 0, trace_maxcl = 0;
   if (trace) {
     if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
@@ -254,7 +324,7 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     return MM_OK;
   };
   if (dtype == MM_F64) {
-    F64Plan pl = f64_plan(m, p, n, ctx->num_sms);
+    F64Plan pl = f64_plan(m, p, n, num_sms);
     if (pl.kb > 1 && (n % 16 != 0 || p % 16 != 0)) pl.kb = 1;  // grouped loads need exact 16-slabs
     mm_status st = ensure_sk(pl.ws_bytes, (size_t)pl.flag_count);
     if (st != MM_OK) return st;
@@ -263,7 +333,11 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     if (st != MM_OK) return st;
     st = encode_2d(ctx, &tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
+#ifdef MM_DIAG
     const bool ftrace = knob("MM_TRACE") != nullptr;
+#else
+    const bool ftrace = false;
+#endif
     if (ftrace) {
       if (!ctx->trace_buf && cudaMalloc(&ctx->trace_buf, 4096 * 48 * sizeof(unsigned long long)) != cudaSuccess)
         return set_err(ctx, MM_ERR_WORKSPACE, "trace buffer allocation failed");
@@ -312,21 +386,21 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
     // ragged last wave they win at burst clocks: the 8-GPU row block of C4 (2048 x 16384 x
     // 16384, 3.46 waves of 512-wide tiles vs 6.92 of 256-wide ones) runs 6 % faster at NT=2.
     const int64_t tiles_nt2 = ((m + 255) / 256) * ((p + 511) / 512);
-    int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= ctx->num_sms / 2)) ? 2 : 1;
+    int nt = (cg == 2 && (a.wave_sync || tiles_nt2 >= num_sms / 2)) ? 2 : 1;
     // two CTA pairs per cluster sharing (multicasting) every B slab
     int mc = 1;
     if (const char* env = knob("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // With few waves of 512-wide tiles (quantisation, an exposed read-out per tile) 256-wide tiles
     // with TMEM double-buffering and two K atoms per stage win: int8 4096^3 +3 %, bf16 4096^3 +2 %;
     // from ~7 waves on (8192^3) 512-wide tiles stay ahead (tools/ab_gpu.py).
-    if (nt == 2 && !a.wave_sync && mc == 1 && tiles_nt2 < 3 * (ctx->num_sms / 2)) nt = 1;
+    if (nt == 2 && !a.wave_sync && mc == 1 && tiles_nt2 < 3 * (num_sms / 2)) nt = 1;
     if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // 256-wide pair tiles: two 128-B K atoms per stage — 8 MMAs per barrier wait and commit instead
     // of 4 (the single issuing thread, not the tensor pipe, bounded 4-MMA stages at ~75 % busy)
     a.ka = (cg == 2 && nt == 1 && n >= 8 * (i8 ? 128 : 64)) ? 2 : 1;
     if (const char* env = knob("MM_KA")) a.ka = (cg == 2 && nt == 1 && atoi(env) == 2) ? 2 : 1;
     size_t ws_bytes = 0, flag_count = 0;
-    tc_plan_needs(i8, cg, nt, mc, a.ka, m, p, n, ctx->num_sms, &ws_bytes, &flag_count);
+    tc_plan_needs(i8, cg, nt, mc, a.ka, m, p, n, num_sms, &ws_bytes, &flag_count);
     mm_status st = ensure_sk(ws_bytes, flag_count);
     if (st != MM_OK) return st;
     tc_box_dims(i8, cg, mc, a.ka, abox, bbox);
@@ -346,10 +420,10 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
                      cbox, "C");
       if (st != MM_OK) return st;
     }
-    e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, a, ctx->num_sms, s);
+    e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, a, num_sms, s);
     trace_nt = nt;
     trace_mc = mc;
-    if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, a.ka, ctx->num_sms);
+    if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, a.ka, num_sms);
   }
   if (e == cudaSuccess) ++ctx->launches;
   if (e == cudaSuccess && trace) {
@@ -512,13 +586,12 @@ __attribute__((visibility("default"))) mm_status mm_create(int device, void* wor
   return MM_OK;
 }
 
-void mm_release_comms(mm_ctx* ctx);  // shard.cu
-
 __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   cudaDeviceSynchronize();
   mm_release_comms(ctx);
+  mm_release_ipc(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_flags) cudaFree(ctx->sk_flags);
@@ -529,6 +602,7 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
     if (b) cudaFree(b);
   if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
   if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+  if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   if (ctx->d_err) cudaFree(ctx->d_err);
   delete ctx;
 }
@@ -540,8 +614,71 @@ __attribute__((visibility("default"))) mm_status mm_gemm(mm_ctx* ctx, int64_t m,
   knobs_refresh();
   DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
+  if (st == MM_OK) st = refuse_diag_knobs(ctx);
   if (st != MM_OK) return st;
   return gemm_ld(ctx, m, n, p, dtype, A, n, B, p, C, p, 0, static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+// Device scratch one product may need (upper bound; SMs <= kSmBound): zero-padded copies of A and B
+// (edge path, as if neither were 16-B pitched), split-tail partial slabs (two slots per CTA) and the
+// per-tile tickets + publish counts.
+constexpr int64_t kSmBound = 160;
+int64_t product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
+  const int64_t ei = (int64_t)dtype_in_size(dt), al = 16 / ei;
+  const int64_t pad = round_up(m * round_up(n, al) * ei, 256) + round_up(n * round_up(p, al) * ei, 256);
+  int64_t slabs, flags;
+  if (dt == MM_F64) {  // 128x128 tiles at most; tiles >= 32x32
+    slabs = kSmBound * 2 * 128 * 128 * 8;
+    flags = 2 * ((m + 31) / 32) * ((p + 31) / 32) * 4;
+  } else {  // CTA slabs of 128 x 512 words at most; tiles >= 128 x 256 per CTA
+    slabs = kSmBound * 2 * 128 * 512 * 4;
+    flags = 2 * ((m + 127) / 128) * ((p + 255) / 256) * 4 * 2;
+  }
+  return pad + round_up(slabs, 256) + round_up(std::max<int64_t>(flags, 256), 256);
+}
+}  // namespace
+
+__attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype,
+                                                                 mm_layout layout, int G) {
+  if (m < 1 || n < 1 || p < 1 || G < 1) return 0;
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return 0;
+  if (layout != MM_ROW_BLOCK && layout != MM_SUMMA_2D && layout != MM_SUMMA_25D) return 0;
+  if (layout != MM_ROW_BLOCK && dtype != MM_F64) return 0;
+  knobs_refresh();
+  int64_t best = 0;
+  auto consider = [&](int pr, int pc, unsigned flags) {
+    for (int r = 0; r < G; ++r) {
+      mm_plan_info info;
+      std::vector<mm_plan_step> steps;
+      if (mm_shard_plan(m, n, p, dtype, layout, pr, pc, flags, 0, G, r, 0, nullptr, 0, &info) != MM_OK) continue;
+      steps.resize((size_t)info.steps);
+      mm_shard_plan(m, n, p, dtype, layout, pr, pc, flags, 0, G, r, 0, steps.data(), info.steps, &info);
+      int64_t total = 512;  // IPC exchange word + barrier word
+      for (int i = 0; i < 4; ++i) total += round_up(std::max<int64_t>(info.stage_bytes[i], 0), 256);
+      int64_t g = 0;
+      for (const mm_plan_step& s : steps)
+        if (s.op == MM_OP_GEMM) g = std::max(g, product_scratch(s.m, s.n, s.p, dtype));
+      best = std::max(best, total + g);
+      if (G == 1) break;
+    }
+  };
+  if (G == 1 && layout == MM_ROW_BLOCK) return (size_t)product_scratch(m, n, p, dtype);
+  if (layout == MM_ROW_BLOCK) {
+    consider(0, 0, MM_BCAST_B);  // staging buffers of the broadcast (the largest variant)
+    consider(0, 0, 0);
+  } else {
+    for (int pr = 1; pr <= G; ++pr) {
+      if (G % pr) continue;
+      const int rest = G / pr;
+      for (int pc = 1; pc <= rest; ++pc) {
+        if (rest % pc) continue;
+        if (layout == MM_SUMMA_2D && pr * pc != G) continue;
+        consider(pr, pc, layout == MM_SUMMA_25D ? (unsigned)MM_REPLICATE : 0u);
+      }
+    }
+  }
+  return (size_t)best;
 }
 
 __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void* stream) {
@@ -574,6 +711,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64
   knobs_refresh();
   DeviceGuard dg(ctx->device);
   mm_status st = validate(ctx, m, n, p, dtype, A, B, C);
+  if (st == MM_OK) st = refuse_diag_knobs(ctx);
   if (st != MM_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t ei = dtype_in_size(dtype), eo = dtype_out_size(dtype);
@@ -602,7 +740,11 @@ __attribute__((visibility("default"))) mm_status mm_gemm_host(mm_ctx* ctx, int64
   const int I = (int)((m + rb - 1) / rb), J = (int)((p + cb - 1) / cb);
   std::vector<cudaEvent_t> evA(I), evB(J), evC((size_t)I * J);
   cudaEvent_t evStart;
+#ifdef MM_DIAG
   const bool trace = knob("MM_HOST_TRACE") != nullptr;  // debug: print the copy/compute timeline
+#else
+  const bool trace = false;
+#endif
   const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
   std::vector<cudaEvent_t> evD((size_t)I * J);
   cudaEventCreateWithFlags(&evStart, evflags);

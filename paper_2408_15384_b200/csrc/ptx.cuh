@@ -134,6 +134,33 @@ __device__ __forceinline__ bool counter_wait(const unsigned* ctr, unsigned targe
   return true;
 }
 
+// Soft wave barrier (sync[0] arrivals, sync[2] "abandoned" flag): waits until *sync >= target
+// for at most `soft_ns`; a persistent grid whose CTAs are not all resident at once (another
+// kernel — an NCCL collective, a concurrent product — holds SMs) would otherwise spin forever.
+// The barrier carries no data dependency (it only aligns the k-phase of a wave for L2 reuse),
+// so on time-out it is abandoned for the rest of the launch: later waits return at once.
+// Never an error.
+#ifndef MMB_SOFT_BARRIER_NS
+#define MMB_SOFT_BARRIER_NS 500000ull  // 0.5 ms (a wave's natural skew is a few microseconds)
+#endif
+__device__ __forceinline__ void soft_wave_wait(unsigned* sync, unsigned target) {
+  if (ld_acquire_gpu(sync + 2) != 0u || ld_acquire_gpu(sync) >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu(sync) < target) {
+    if (ld_acquire_gpu(sync + 2) != 0u) return;
+    __nanosleep(32);
+    if (globaltimer_ns() - t0 > MMB_SOFT_BARRIER_NS) {
+      atomicExch(sync + 2, 1u);
+      return;
+    }
+  }
+}
+__device__ __forceinline__ unsigned atomic_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // L2-only (.cg) global loads/stores for the split-tile partials.  asm volatile with a memory
 // clobber: CUDA's __ldcg/__stcg are plain (non-volatile, clobber-free) asm, which the compiler may
 // move across the flag wait / named barrier that order them with the other CTA — it did: a

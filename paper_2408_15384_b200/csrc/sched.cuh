@@ -12,16 +12,16 @@ namespace mmb {
 // grouped raster), then the tiles of the last, partial wave are split stream-K
 // style: their (tile, k-block) iterations are cut into ntc equal ranges, one per
 // cluster, so no SM idles through a ragged last wave (C3: 3.46 waves -> 3 + an
-// even tail; C4: 55.35 -> 55 + tail).  A split tile is finished by the cluster
-// holding its k-block 0 (the last segment of that cluster's range); the others
-// (the first segment of theirs) publish partial tiles and bump a counter; the
-// finisher adds them in cluster order (fixed order: deterministic).
+// even tail; C4: 55.35 -> 55 + tail).  The parts of a split tile take tickets as
+// they finish; every part but the last publishes its partial tile, the last adds
+// them in segment order (fixed order: deterministic).  No part waits for a cluster
+// that may not have started, so the grid never relies on co-residency.
 struct WorkSched {
   int tiles_m, tiles_n, group_m, num_kb;
   int nc;    // clusters
   int W;     // full data-parallel waves
   int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
-  int land;  // tail tiles split in exact halves: the finisher lands the partner's slab in its idle stage ring
+  int land;  // tail tiles split in exact halves: the last half lands the other's slab in its idle stage ring
   int red;   // tail tiles split in exact halves, both adding into C (zeroed first) by TMA reduce-add stores
   int64_t TI;  // tail iterations = tail tiles * num_kb
 
@@ -92,7 +92,7 @@ inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, 
     s.ntc = 0;
     s.TI = 0;
   } else if (tail_mode >= 2) {
-    s.ntc = (int)(2 * tail);  // exact halves: finisher + one contributor per tile
+    s.ntc = (int)(2 * tail);  // exact halves: two parts per tile
     s.land = tail_mode == 2;
     s.red = tail_mode == 3;
   } else {

@@ -106,3 +106,35 @@ def test_summa_panels_cover_and_respect_blocks(n, pr, pc, panel):
         assert s <= k0 and k0 + kw <= s + c
         k += kw
     assert k == n
+
+
+def test_workspace_size_bound():
+    """mm_workspace_size through the C-ABI: 0 for invalid arguments; at least the
+    zero-padded operand copies of the edge path; grows with the shape; the sharded layouts add
+    their panel staging (G > 1) — pure host logic, no device."""
+    lib = _lib.load()
+    f = lib.mm_workspace_size
+    assert f(0, 4, 4, 0, 0, 1) == 0 and f(4, 4, 4, 7, 0, 1) == 0 and f(4, 4, 4, 0, 9, 1) == 0
+    assert f(4, 4, 4, 1, 1, 2) == 0  # SUMMA layouts are FP64 only
+    for dt, esz in ((0, 8), (1, 2), (2, 1)):
+        small, big = f(300, 200, 100, dt, 0, 1), f(3000, 2000, 1000, dt, 0, 1)
+        assert small > 0 and big > small
+        al = 16 // esz
+        pad = (3000 * (-(-2000 // al) * al) + 2000 * (-(-1000 // al) * al)) * esz
+        assert big >= pad
+    # row-block with G ranks: the B broadcast stages two column panels of B (p/8 wide each)
+    n, p = 4096, 4096
+    assert f(4096, n, p, 1, 0, 8) >= 2 * n * (p // 8) * 2
+    # SUMMA: two panel sets, the largest over the grids G factors into
+    assert f(8192, 8192, 8192, 0, 1, 8) >= 2 * (8192 * 2048 * 8)
+    assert mm.workspace_size(16384, 16384, 16384, torch.bfloat16) == f(16384, 16384, 16384, 1, 0, 1)
+
+
+def test_diag_knobs_refused_by_release_build(monkeypatch):
+    """MM_DEBUG (skips loads/stores: garbage results) and MM_TRACE / MM_HOST_TRACE (hidden stream
+    synchronisations) exist only in the diagnostic build; the release library refuses them with
+    MM_ERR_UNSUPPORTED before touching the device.  Checked here on the release .so's strings and in
+    tests/test_gpu_parity.py on the device."""
+    out = subprocess.run(["strings", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "is a diagnostic knob of the diagnostic build only" in out
+    assert "[mm trace]" not in out  # the timeline printers are compiled out of the release library

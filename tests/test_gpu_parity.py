@@ -478,8 +478,8 @@ def test_epilogue_guard_bands_both_tile_widths(mm, dt):
             mm.gemm(to_dev(A, dt), to_dev(B, dt), out=C)
             mm.sync_check()
             h = buf.cpu().numpy()
-            assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), (m, n, p, epi)
-            assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p, epi)
+            assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), (m, n, p, nt)
+            assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p, nt)
     finally:
         os.environ.pop("MM_NT", None)
 
@@ -713,14 +713,20 @@ def test_config4_fp64_32768_exact_pin(mm):
 
 
 def test_config4_fp64_32768_sampled(mm):
-    """configs[4] at full size on one GPU (the SUMMA G=1 reference), oracle on sampled rows/cols."""
+    """configs[4] at full size on one GPU (the SUMMA G=1 reference), oracle on sampled rows/cols
+    (>= 64 seeded rows and >= 64 seeded columns, plus the SUMMA grid's block
+    boundaries — rows of the 2-row-block grids, columns of the 2- and 4-column-block grids of
+    configs[4] at G = 2/4/8 — and the first/last row and column)."""
     N = 32768
     A, B = gen("f64", "random", 4, N, N, N)
     Ad, Bd = to_dev(A, "f64"), to_dev(B, "f64")
     C = mm.gemm(Ad, Bd)
     mm.sync_check()
-    rows = _sample(N, 6, 3, 4, [0, N - 1, 16383, 16384])
-    cols = _sample(N, 6, 4, 4, [0, N - 1, 16383])
+    row_seams = [0, N - 1, 16383, 16384]
+    col_seams = [0, N - 1] + [b + d for b in (8192, 16384, 24576) for d in (-1, 0)]
+    rows = _sample(N, 64, 3, 4, row_seams)
+    cols = _sample(N, 64, 4, 4, col_seams)
+    assert rows.size >= 64 + len(row_seams) - 2 and cols.size >= 64 + len(col_seams) - 2
     Crow = C[torch.from_numpy(rows).cuda()].cpu().numpy()
     Ccol = C[:, torch.from_numpy(cols).cuda()].cpu().numpy()
     del C, Ad, Bd
