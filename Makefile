@@ -55,3 +55,9 @@ HOG_LIB := tests/libhog.so
 all: $(HOG_LIB)
 $(HOG_LIB): tests/csrc/hog.cu
 	$(NVCC) -std=c++17 -O2 $(GENCODE) -Xcompiler -fPIC -shared -o $@ $<
+
+# K6 MMA-only peak probes (measured flop/clk/SM; bench.py)
+K6_LIB := probes/libk6.so
+all: $(K6_LIB)
+$(K6_LIB): probes/k6_peak.cu paper_2408_15384_b200/csrc/ptx.cuh
+	$(NVCC) -std=c++17 -O3 $(GENCODE) -Ipaper_2408_15384_b200/csrc -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -o $@ $<
