@@ -53,6 +53,18 @@ WORKLOAD = ("BASELINE.json configs[3]: BF16 16384x16384 . 16384x16384, FP32 accu
             "entries Box-Muller N(0,1) rounded to bf16 from seed 3, row-major")
 
 
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
+
+
+TRAFFIC_ALL = load_traffic()
+TRAFFIC = TRAFFIC_ALL.get("per_config", {})
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -62,77 +74,167 @@ def load_peaks():
     return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
 
 
-def cpu_count_used():
-    import oracle
-    return oracle.max_threads()
+def host_cpu_info():
+    """lscpu model / sockets / cores, and the CPUs this process may run on."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=20).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            info[k.strip()] = v.strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+
+    def num(key, default):
+        try:
+            return int(info.get(key, default))
+        except ValueError:
+            return default
+    usable = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    sockets, cps, tpc = num("Socket(s)", 1), num("Core(s) per socket", usable), num("Thread(s) per core", 1)
+    physical = sockets * cps
+    return {"model": info.get("Model name", "unknown"), "sockets": sockets, "cores_per_socket": cps,
+            "threads_per_core": tpc, "logical_cpus": num("CPU(s)", usable), "usable_cpus": usable,
+            "physical_cores": physical, "parallel_threads": max(1, min(physical, usable))}
 
 
-def oracle_rows_sample(A_bits, B_bits, nrows, seed=7):
-    """Time the oracle (as it stands) on `nrows` full rows of C; returns (seconds, flops)."""
+# Work each oracle-baseline mode times (BASELINE.json configs; SURVEY 8(d) d7): "full" products, or
+# the first R rows of C (the same loops over an R-row A: time per row does not depend on which row),
+# extrapolated to the full product and labelled so.
+ORACLE_WORK = {
+    "serial": {"C1": 0, "C2": 0, "C3": 64, "C4": 1, "C5": 1},
+    "parallel": {"C1": 0, "C2": 0, "C3": 0, "C4": "2T", "C5": "T"},
+}
+CONFIG_SHAPES = {"C1": ("f64", 256, 256, 256, 0), "C2": ("f64", 2000, 1500, 1750, 1), "C3": ("i8", 4096, 4096, 4096, 2),
+                 "C4": ("bf16", 16384, 16384, 16384, 3), "C5": ("f64", 32768, 32768, 32768, 4)}
+
+
+def oracle_worker(mode, threads):
+    """`bench.py --oracle-worker MODE --threads T`: the CPU oracle (oracle/, as it stands) timed in a
+    fresh process that loads nothing but numpy, oracle/ and synthgen/ (no torch, no CUDA context),
+    with OpenMP threads bound to cores.  Prints one JSON line."""
+    import ctypes
     import oracle
     import synthgen as sg
-    rows = np.unique(sg.sample_indices(seed, sg.ROLE_ROWS, nrows, A_bits.shape[0]))
-    t0 = time.perf_counter()
-    oracle.gemm_bf16_rows(A_bits, B_bits, rows)
-    dt = time.perf_counter() - t0
-    return dt, 2.0 * rows.size * A_bits.shape[1] * B_bits.shape[1], rows.size
+    gomp = ctypes.CDLL("libgomp.so.1")  # the OpenMP runtime oracle/ and synthgen/ share
+    usable = len(os.sched_getaffinity(0))
+    out = {"mode": mode, "threads": threads}
+    for cfg, spec in ORACLE_WORK[mode].items():
+        dt, m, n, p, seed = CONFIG_SHAPES[cfg]
+        rows = m if spec == 0 else (2 * threads if spec == "2T" else threads if spec == "T" else int(spec))
+        gomp.omp_set_num_threads(usable)  # input generation is not timed: all CPUs
+        if dt == "f64":
+            A, B = sg.uniform_f64(seed, sg.ROLE_A, rows, n), sg.uniform_f64(seed, sg.ROLE_B, n, p)
+            fn = lambda: oracle.gemm_f64(A, B)  # noqa: E731
+        elif dt == "bf16":
+            A, B = sg.normal_bf16(seed, sg.ROLE_A, rows, n), sg.normal_bf16(seed, sg.ROLE_B, n, p)
+            fn = lambda: oracle.gemm_bf16(A, B)  # noqa: E731
+        else:
+            A, B = sg.uniform_i8(seed, sg.ROLE_A, rows, n), sg.uniform_i8(seed, sg.ROLE_B, n, p)
+            fn = lambda: oracle.gemm_s8(A, B)  # noqa: E731
+        gomp.omp_set_num_threads(threads)
+        assert oracle.max_threads() == threads
+        reps = 3 if 2.0 * rows * n * p < 1e9 else 1
+        best = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        flops = 2.0 * rows * n * p
+        full = 2.0 * m * n * p
+        out[cfg] = {"dtype": dt, "shape": [m, n, p], "rows_timed": rows, "seconds": round(best, 4),
+                    "gflops": round(flops / best / 1e9, 3),
+                    "full_product_seconds": round(best if rows == m else full / (flops / best), 2),
+                    "full_product": "measured" if rows == m else f"extrapolated from {rows} of {m} rows"}
+        del A, B
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def oracle_baseline(modes=("serial", "parallel")):
+    """Run oracle_worker in clean subprocesses (serial, and all physical cores) -> dict."""
+    cpu = host_cpu_info()
+    res = {"host": cpu}
+    for mode in modes:
+        T = 1 if mode == "serial" else cpu["parallel_threads"]
+        env = dict(os.environ, OMP_NUM_THREADS=str(T), OMP_PROC_BIND="close", OMP_PLACES="cores")
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker", mode, "--threads", str(T)],
+                               capture_output=True, text=True, env=env, timeout=900)
+            lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+            res[mode] = json.loads(lines[-1]) if lines else {"error": r.stderr[-300:]}
+        except subprocess.TimeoutExpired:
+            res[mode] = {"error": "timeout"}
+    return res
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md recipe)."""
+    """nvidia-smi clocks/throttle sampling (B200_PROFILING.md recipe) every 20 ms; every sample
+    carries the host time it arrived, so summary(t0, t1) keeps only samples taken inside a timed
+    region (idle samples before/after it do not dilute the median)."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.samples = []  # (host time, line)
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)  # nvidia-smi start-up: the first samples arrive after ~0.1-0.2 s
         except (OSError, FileNotFoundError):
             self.proc = None
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.time(), line.strip()))
 
     def stop(self):
-        if not self.proc:
-            return None
-        time.sleep(0.12)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        """Median SM clock, max clock, power and throttle reasons of the samples in [t0, t1]."""
+        sm, mx, pw, reasons = [], 0.0, [], set()
+        for (ts, ln) in self.samples:
+            if (t0 is not None and ts < t0) or (t1 is not None and ts > t1 + 0.025):
+                continue
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx = max(mx, float(parts[1]))
+                pw.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
+            for nm, v in zip(self.NAMES, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(pw) if pw else None,
+                "window": "samples inside the timed region only (host-timestamped, 20 ms period)"}
 
 
-def device_time_steps(fn, steps, warmup, dist=None):
-    """Max-over-ranks device time (ms) per step of `fn` on the current stream."""
+def device_time_steps(fn, steps, warmup, dist=None, window=None):
+    """Max-over-ranks device time (ms) per step of `fn` on the current stream.  `window`, a list,
+    receives the host times bracketing the timed region (for the clock samples)."""
     import torch
     for _ in range(warmup):
         fn()
@@ -142,11 +244,14 @@ def device_time_steps(fn, steps, warmup, dist=None):
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
     e0.record(s)
     for _ in range(steps):
         fn()
     e1.record(s)
     torch.cuda.synchronize()
+    if window is not None:
+        window[:] = [t0, time.time()]
     ms = e0.elapsed_time(e1)
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -201,7 +306,43 @@ def graph_us(fn, n=100, reps=5):
     return statistics.median(ts)
 
 
-def per_config_table(mm, peaks):
+def k6_peaks():
+    """K6 MMA-only probes (probes/libk6.so): measured flop (int op) per clock per SM of tcgen05
+    kind::f16 / kind::i8 (M=256 N=256, CTA pair) and DMMA.8x8x4 (SURVEY 8(d) d4 (iii))."""
+    import ctypes
+    path = os.path.join(ROOT, "probes", "libk6.so")
+    if not os.path.exists(path):
+        return None
+    lib = ctypes.CDLL(path)
+    lib.k6_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    out = {}
+    for kind, name, iters in ((0, "bf16", 8192), (1, "i8", 8192), (2, "f64", 4000)):
+        f, c, t = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        st = lib.k6_run(kind, iters, 5, ctypes.byref(f), ctypes.byref(c), ctypes.byref(t))
+        if st == 0:
+            out[name] = {"flop_per_clk_sm": round(f.value, 1), "probe_clock_mhz": round(c.value, 1),
+                         "tflops_at_probe_clock": round(t.value, 1)}
+        else:
+            out[name] = {"error": st}
+    out["how"] = ("back-to-back MMAs on smem/register operands, no loads or epilogue, every SM; per-SM "
+                  "clock64 over the loop (zero operands: ops/clk is data-independent, the clock is not)")
+    return out
+
+
+def flop_per_clk(k6, dt, nominal):
+    try:
+        return float(k6[dt]["flop_per_clk_sm"]), "measured (K6 probe)"
+    except (TypeError, KeyError, ValueError):
+        return float(nominal), "nominal (K6 probe unavailable)"
+
+
+def compulsory_bytes(dt, m, n, p):
+    ei, eo = {"f64": (8, 8), "bf16": (2, 4), "i8": (1, 4)}[dt]
+    return (m * n + n * p) * ei + m * p * eo
+
+
+def per_config_table(mm, peaks, k6=None):
     """Brief timings of the other BASELINE.json configs at N=1 (ours vs cuBLAS)."""
     import torch
     from synthgen import gpu as sgg  # the synthgen recipe evaluated on the GPU (bit-identical)
@@ -253,19 +394,27 @@ def per_config_table(mm, peaks):
             C = torch.empty(m, p, device="cuda", dtype=torch.float64 if dt == "f64" else torch.int32)
             flops = 2.0 * m * n * p
             big = m * n > (1 << 26)
-            ck = ClockSampler()
-            ck.start()
+            ck = ClockSampler().start()
+            w0 = time.time()
             t_ours = per_launch_ms(lambda: mm.gemm(A, B, out=C), reps, None if big else flush)
-            clk_ours = ck.stop()
-            mm.sync_check()
-            ck = ClockSampler()
-            ck.start()
+            w1 = time.time()
             t_ref = per_launch_ms(ref, reps, None if big else flush)
-            clk_ref = ck.stop()
+            w2 = time.time()
+            ck.stop()
+            clk_ours, clk_ref = ck.summary(w0, w1), ck.summary(w1, w2)
+            mm.sync_check()
             tf = flops / t_ours / 1e9
-            # SMs x flop/clk/SM x the SM clock sampled while it ran
-            opc = OPS_PER_CLK_SM["f64" if dt == "f64" else "i8"]
+            # SMs x flop/clk/SM (K6-measured) x the SM clock sampled while it ran
+            opc, opc_src = flop_per_clk(k6, "f64" if dt == "f64" else "i8", OPS_PER_CLK_SM["f64" if dt == "f64" else "i8"])
             clock_peak = (SMS * opc * clk_ours["sm_mhz"] * 1e6 / 1e12) if clk_ours else None
+            cb = compulsory_bytes(dt, m, n, p)
+            dram = (TRAFFIC.get(name) or {}).get("dram_bytes_per_launch")
+            hbm = {"compulsory_bytes": cb, "algorithmic_gbs": round(cb / (t_ours * 1e-3) / 1e9, 1),
+                   "ncu_dram_bytes_per_launch": dram,
+                   "ncu_dram_gbs": round(dram / (t_ours * 1e-3) / 1e9, 1) if dram else None,
+                   "peak_gbs": peaks.get("hbm_gbs"),
+                   "note": "algorithmic = (mn+np)·s_in + mp·s_out per launch / kernel time; ncu = dram bytes "
+                           "read+written by one launch (profiles/traffic.json, cold L2) / the same time"}
             lib = lib_peaks.get(dt)
             graph = None
             if m * n * p <= (1 << 27):
@@ -278,6 +427,7 @@ def per_config_table(mm, peaks):
                 "peak": round(nominal, 1), "peak_note": peak_note,
                 "frac_of_library_peak": round(tf / lib, 4) if lib else None,
                 "frac_of_clock_peak": round(tf / clock_peak, 4) if clock_peak else None,
+                "clock_peak_flop_per_clk_sm": opc, "clock_peak_source": opc_src, "hbm": hbm,
                 "sm_mhz": clk_ours["sm_mhz"] if clk_ours else None,
                 "cublas_sm_mhz": clk_ref["sm_mhz"] if clk_ref else None,
                 "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
@@ -291,31 +441,37 @@ def per_config_table(mm, peaks):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on this host (rank 0 only)."""
+    """--impl reference: the CPU oracle (oracle/, as it stands) on this host's physical cores
+    (OpenMP threads bound to cores), on bounded row samples of the C4 workload (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    cpu = host_cpu_info()
+    T = cpu["parallel_threads"]
+    os.environ.update(OMP_NUM_THREADS=str(T), OMP_PROC_BIND="close", OMP_PLACES="cores")  # before liboracle loads
+    import oracle
     import synthgen as sg
-    A = sg.normal_bf16(SEED, sg.ROLE_A, M, N_)
+    rows_per_step = 2 * T
+    A = sg.normal_bf16(SEED, sg.ROLE_A, rows_per_step, N_)  # rows 0..R-1 of A (time per row is row-independent)
     B = sg.normal_bf16(SEED, sg.ROLE_B, N_, P)
-    cores = cpu_count_used()
-    nrows = max(8, cores)
-    for i in range(args.warmup):
-        oracle_rows_sample(A, B, max(1, cores // 2), seed=100 + i)
-    secs, flops, rows = 0.0, 0.0, 0
-    for i in range(args.steps):
-        dt, fl, nr = oracle_rows_sample(A, B, nrows, seed=200 + i)
-        secs += dt
-        flops += fl
-        rows += nr
+    for _ in range(args.warmup):
+        oracle.gemm_bf16(A[:max(1, T // 2)], B)
+    secs = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.gemm_bf16(A, B)
+        secs += time.perf_counter() - t0
+    flops = 2.0 * rows_per_step * N_ * P * args.steps
     value = flops / secs / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16->f64 (oracle)",
         "data": "synthetic", "config": {"workload": WORKLOAD, "m": M, "n": N_, "p": P, "seed": SEED},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{rows} full rows of C ({nrows} per step, seeded) of the 16384^3 product"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                         "host": cpu,
+                         "sample": f"{rows_per_step} full rows of C per step ({args.steps} steps) of the 16384^3 BF16 "
+                                   f"product, OpenMP threads bound to physical cores"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -331,7 +487,12 @@ def main():
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-protocol", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--threads", type=int, default=1, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.oracle_worker:
+        return oracle_worker(args.oracle_worker, args.threads)
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
@@ -362,24 +523,39 @@ def main():
     del A_dev_full
     A_host = A.view(torch.int16).cpu().numpy().view(np.uint16)
     B_host = B.view(torch.int16).cpu().numpy().view(np.uint16)
-    A_full = A_host  # the cpu_baseline runs at N=1 only, where A_host is all of A
     C = torch.empty(rows, P, dtype=torch.float32, device="cuda")
     flops_total = 2.0 * M * N_ * P
 
+    # K6 MMA-only probes (measured flop/clk/SM), before the product so its clocks are not disturbed
+    k6 = k6_peaks() if rank == 0 else None
     launches0 = mm.launches()
-    clk = ClockSampler(local)
     step = (lambda: mm.gemm(A, B, out=C)) if rows > 0 else (lambda: None)
-    # warm-up, then the timed region with clocks sampled during it
+    # warm-up, then the timed region with clocks sampled during it (samples outside it are dropped)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clk.start()
-    time.sleep(0.2)
-    ms = device_time_steps(step, args.steps, 0, dist)
-    clocks = clk.stop()
+    clk = ClockSampler(local).start()
+    win = []
+    ms = device_time_steps(step, args.steps, 0, dist, window=win)
+    clk.stop()
+    clocks = clk.summary(*win)
     mm.sync_check()
     launches = mm.launches() - launches0 - args.warmup * (1 if rows > 0 else 0)
     value = flops_total / (ms * 1e-3) / 1e12
+
+    # ---- sustained: back-to-back steps for >= 2 s (the burst headline above is the first K steps)
+    sustained = None
+    if rows > 0 and not args.no_sustained:
+        n_sus = max(args.steps, int(2000.0 / max(ms, 1e-3)) + 1)
+        ck = ClockSampler(local).start()
+        w2 = []
+        ms_sus = device_time_steps(step, n_sus, 0, dist, window=w2)
+        ck.stop()
+        mm.sync_check()
+        sustained = {"steps": n_sus, "seconds": round(ms_sus * n_sus / 1e3, 2), "ms_per_step": round(ms_sus, 4),
+                     "value": round(flops_total / (ms_sus * 1e-3) / 1e12, 2), "unit": UNIT, "clocks": ck.summary(*w2),
+                     "frac_of_sustained_peak": round(flops_total / world / (ms_sus * 1e-3) / 1e12 /
+                                                     peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), 4)}
 
     # ---- context: cuBLAS on the same operands and the same bf16 -> fp32 product (torch.mm out_dtype),
     # back-to-back like the timed steps above (sustained regime); not part of the result
@@ -506,16 +682,21 @@ def main():
 
     per_config = None
     if rank == 0 and not args.no_per_config:
-        per_config = per_config_table(mm, peaks)
+        per_config = per_config_table(mm, peaks, k6)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = cpu_count_used()
-        nrows = max(8, 2 * cores)
-        secs, fl, nr = oracle_rows_sample(A_full, B_host, nrows)
-        cpu_baseline = {"value": fl / secs / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
-                        "sample": f"{nr} seeded full rows of C of the 16384^3 BF16 product "
-                                  f"({fl/1e9:.1f} GFLOP, {secs:.1f} s)"}
+        ob = oracle_baseline()
+        par = ob.get("parallel", {}).get("C4") or {}
+        cpu_baseline = {"value": par.get("gflops", 0.0) / 1e3, "unit": UNIT,
+                        "cores": ob.get("parallel", {}).get("threads"), "kind": "oracle",
+                        "sample": (f"{par.get('rows_timed')} full rows of C of the 16384^3 BF16 product (first rows of "
+                                   f"A; {par.get('seconds')} s) in a fresh process (no torch/CUDA), OpenMP threads "
+                                   f"bound to physical cores; full product {par.get('full_product_seconds')} s "
+                                   f"({par.get('full_product')})"),
+                        "host": ob.get("host"), "modes": {k: v for k, v in ob.items() if k != "host"},
+                        "note": "serial = 1 thread; parallel = all physical cores; C1-C3 full products timed "
+                                "(C3 serial: 64 rows), C4/C5 row samples extrapolated and labelled"}
 
     if rank == 0:
         line = {
@@ -526,17 +707,19 @@ def main():
                        "parallelism": f"row-block x{world} (B resident on every rank)" if world > 1 else "single GPU",
                        "l2": "operands larger than L2 (A+B 1 GiB, C 1 GiB vs 126 MB): no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "with_comm": with_comm, "library_baseline": library, "per_config": per_config,
+            "clocks": clocks, "sustained": sustained, "k6_peaks": k6,
+            "with_comm": with_comm, "library_baseline": library, "per_config": per_config,
             "protocol": protocol,
             "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
                                        "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
                                        "vs_spec_2250": round(value / world / 2250.0, 4),
                                        "vs_clock_normalized": (round(value / world / (
                                            torch.cuda.get_device_properties(0).multi_processor_count *
-                                           OPS_PER_CLK_SM["bf16"] * clocks["sm_mhz"] * 1e6 / 1e12), 4)
-                                           if clocks else None),
-                                       "clock_normalized_note": "SMs x 8192 flop/clk x median nvidia-smi SM clock "
-                                                                "of the timed region"},
+                                           flop_per_clk(k6, "bf16", OPS_PER_CLK_SM["bf16"])[0] * clocks["sm_mhz"]
+                                           * 1e6 / 1e12), 4) if clocks else None),
+                                       "clock_normalized_note": "SMs x flop/clk/SM (" +
+                                           flop_per_clk(k6, "bf16", OPS_PER_CLK_SM["bf16"])[1] +
+                                           ") x median nvidia-smi SM clock of samples inside the timed region"},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
