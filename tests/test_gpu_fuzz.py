@@ -23,11 +23,13 @@ KNOBS_TC = {
     "MM_KA": [None, "1"],
     "MM_FORCE_CG": [None, "1", "2"],
     "MM_MC": [None, None, "2"],
+    "MM_L2_HINT": [None, None, None, "1", "3"],
+    "MM_WAVE_SYNC": [None, None, None, "2"],
 }
 KNOBS_F64 = {
     "MM_F64_TILE": [None, "32", "64", "128"],
     "MM_F64_STREAMK": [None, "0", "1"],
-    "MM_F64_W8": [None, None, "1"],
+    "MM_F64_W8": [None, None, None, "1"],
 }
 
 
