@@ -736,6 +736,7 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   if (tail > 0 && mc == 1 && 2 * tail <= nc && K >= (i8 ? 4608 : 2304))
     mode = c_tma ? 3 : ((!i8 && nt == 1 && num_kb >= 8) ? 2 : 0);
   if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
+  if (knob("MM_ONE_TILE")) return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)T, 0);  // (A/B knob: one tile per cluster, non-persistent)
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
   if (mode == 2 && (nt != 1 || 2 * tail > nc)) mode = 1;  // landing: 256-wide tiles, one partner per tile
   if (mode == 3 && (!c_tma || 2 * tail > nc)) mode = 1;
