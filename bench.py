@@ -134,7 +134,8 @@ def oracle_worker(mode, threads):
             fn = lambda: oracle.gemm_s8(A, B)  # noqa: E731
         gomp.omp_set_num_threads(threads)
         assert oracle.max_threads() == threads
-        reps = 3 if 2.0 * rows * n * p < 1e9 else 1
+        fn()  # warm-up (thread pool, first touch of the output): the reference arm also warms up
+        reps = 3 if 2.0 * rows * n * p < 1e9 else 2
         best = float("inf")
         for _ in range(reps):
             t0 = time.perf_counter()
@@ -488,6 +489,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-protocol", action="store_true")
     ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--no-k6", action="store_true")
     ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--threads", type=int, default=1, help=argparse.SUPPRESS)
     args = ap.parse_args()
@@ -527,7 +529,7 @@ def main():
     flops_total = 2.0 * M * N_ * P
 
     # K6 MMA-only probes (measured flop/clk/SM), before the product so its clocks are not disturbed
-    k6 = k6_peaks() if rank == 0 else None
+    k6 = k6_peaks() if rank == 0 and not args.no_k6 else None
     launches0 = mm.launches()
     step = (lambda: mm.gemm(A, B, out=C)) if rows > 0 else (lambda: None)
     # warm-up, then the timed region with clocks sampled during it (samples outside it are dropped)

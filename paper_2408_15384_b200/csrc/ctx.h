@@ -27,7 +27,7 @@ struct mm_ctx {
   bool ev_last_valid = false;
   void* ws = nullptr;  // internal, grow-only (padding path)
   size_t ws_bytes = 0;
-  int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..3] wave-barrier counters + abandoned flag
+  int* d_err = nullptr;  // [0] device error word (pipeline timeouts), [1..4] wave-barrier / pacing counters, abandoned flag
   int wave_sync = 1;
   // mm_gemm_host staging
   void* hbuf[3] = {nullptr, nullptr, nullptr};

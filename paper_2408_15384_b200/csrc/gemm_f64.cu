@@ -48,7 +48,11 @@ constexpr int BBOX_BYTES = BK * 16 * 8;  // 2 KB, box {16 cols, 16 rows}
 // k-blocks into KB consecutive ring slots, so a 32x32 tile's whole K arrives in a few loads — a
 // single thread issuing three 2-D loads per 16-deep k-block was the bottleneck at C1: ~160
 // cycles per load).  B then sits per group as [column box][KB x 16 rows][128 B].
-template <int BM, int BN, int WM, int WN, int KS = 1, int KB = 1>
+// CK: CTAs per tile along K (a cluster of CK CTAs on CK SMs; CK = 2 for problems with at most half
+// a wave of 32x32 tiles, e.g. C1: 64 tiles on 128 SMs instead of 64).  Rank 1 adds nothing itself:
+// it stores its partial tile into rank 0's shared memory (distributed shared memory) and arrives on
+// rank 0's exchange barrier; rank 0 adds it to its own (fixed order) and writes C.
+template <int BM, int BN, int WM, int WN, int KS = 1, int KB = 1, int CK = 1>
 struct F64Cfg {
   static constexpr int NTILE = WM * WN;        // warps covering one tile
   static constexpr int NCONS = NTILE * KS;     // consumer warps
@@ -63,7 +67,8 @@ struct F64Cfg {
   static constexpr int STAGES = STAGES0 / KB * KB;            // whole groups of KB slots
   static constexpr int BOX_STRIDE = KB * BBOX_BYTES;          // between B column boxes of one slot
   static constexpr int SCR_BYTES = (KS - 1) * BM * BN * 8;  // accumulators of groups 1..KS-1
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + 1024;
+  static constexpr int XSCR_BYTES = (CK - 1) * BM * BN * 8;  // rank 0: the other K half's partial tile
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + XSCR_BYTES + 1024;
   static_assert(STAGES >= 4 && 16 * STAGES <= 1008, "ring (+ the ticket word at the end of the barrier area)");
   static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
   static constexpr int NI = BN / WN / 8;  // 8-col DMMA tiles per warp (even: pairs share a 16-col box)
@@ -72,12 +77,12 @@ struct F64Cfg {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int BM, int BN, int WM, int WN, int KS, int KB>
-__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
+template <int BM, int BN, int WM, int WN, int KS, int KB, int CK>
+__global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB, CK>::THREADS, 1)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3, GemmArgs args,
                     WorkSched sched) {
-  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB>;
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB, CK>;
   // optional per-CTA timeline (MM_TRACE=1), globaltimer ns: [0] entry, [1] prologue done, [2] first
   // load issued, [3] first stage landed (consumer warp 0), [4] first item's k-loop done, [5] first
   // item stored, [6] exit
@@ -99,7 +104,17 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int c = blockIdx.x;
+  const int c = CK == 1 ? (int)blockIdx.x : (int)blockIdx.x / CK;  // schedule unit: CTA, or cluster (CK > 1)
+  const uint32_t krank = CK == 1 ? 0u : __shfl_sync(0xffffffffu, cluster_ctarank(), 0);  // K part of the tile
+  const uint32_t xbar = bar0 + 16u * STAGES;  // (CK > 1, rank 0) exchange barrier: rank 1's partial has landed
+  // (CK > 1) this CTA's part of a whole tile's k-blocks: halves rounded to whole KB groups
+  auto k_part = [&](int& kb0, int& kb1) {
+    if constexpr (CK > 1) {
+      const int h = ((kb1 - kb0 + 1) / 2 + KB - 1) / KB * KB;
+      if (krank == 0) kb1 = min(kb1, kb0 + h);
+      else kb0 = min(kb1, kb0 + h);
+    }
+  };
   const int num_kb = sched.num_kb;
   int* err = args.err;
 
@@ -117,9 +132,10 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
       // per group of KB slots (on its first slot's barrier)
       mbar_init(empty_bar(s), KB == 1 ? NTILE : NCONS);
     }
+    if (CK > 1) mbar_init(xbar, NTILE * 32);  // one arrival per thread of rank 1's tile warps
     fence_mbar_init();
   }
-  __syncthreads();
+  if constexpr (CK > 1) cluster_sync(); else __syncthreads();
   if (tl && threadIdx.x == 0) tl[1] = globaltimer_ns();
 
   if (warp == NCONS) {
@@ -133,6 +149,7 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
       for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
         int tm, tn;
         sched.tile_coords(t, tm, tn);
+        k_part(kb0, kb1);
         for (int kb = kb0; kb < kb1; kb += KB) {
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 11)) { ok = false; break; }
           mbar_arrive_expect_tx(full_bar(stage), KB * Cfg::STAGE_BYTES);
@@ -188,6 +205,8 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
     for (int j = 0; ok && sched.item(c, j, t, kb0, kb1); ++j) {
       int tm, tn;
       sched.tile_coords(t, tm, tn);
+      const bool whole = (kb0 == 0 && kb1 == num_kb);  // (of the tile; CK > 1 splits only whole tiles)
+      k_part(kb0, kb1);
       double acc[Cfg::MI][Cfg::NI][2];
 #pragma unroll
       for (int mi = 0; mi < Cfg::MI; ++mi)
@@ -279,8 +298,36 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
         named_bar(3, NCONS * 32);
         if (kgrp != 0) continue;  // group 0 finishes the tile
       }
+      if constexpr (CK > 1) {
+        // the tile's K halves: rank 1 stores its partial into rank 0's exchange buffer (distributed
+        // shared memory), each thread then arrives (release, cluster scope) on rank 0's barrier;
+        // rank 0 waits (acquire) and adds: acc(rank 0's k-blocks) + acc(rank 1's) — fixed order
+        const uint32_t xs = smem_u32(smem + STAGES * Cfg::STAGE_BYTES + 1024 + Cfg::SCR_BYTES);
+        if (krank != 0) {
+          const uint32_t rx = mapa_shared(xs, 0);
+#pragma unroll
+          for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < Cfg::NI; ++ni) {
+              const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+              st_cluster_d2(rx + (uint32_t)(r * BN + cc) * 8u, acc[mi][ni][0], acc[mi][ni][1]);
+            }
+          mbar_arrive_cluster(mapa_shared(xbar, 0));
+          continue;  // rank 0 writes the tile
+        }
+        if (!mbar_wait_cluster(xbar, 0, args.err, 14)) { ok = false; break; }
+#pragma unroll
+        for (int mi = 0; mi < Cfg::MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < Cfg::NI; ++ni) {
+            const int r = wm * (BM / WM) + mi * 8 + arow, cc = wn * (BN / WN) + (ni >> 1) * 16 + (ni & 1) * 4 + dcol;
+            const double2 v = *reinterpret_cast<const double2*>(smem + STAGES * Cfg::STAGE_BYTES + 1024 + Cfg::SCR_BYTES +
+                                                               (size_t)(r * BN + cc) * 8);
+            acc[mi][ni][0] += v.x;
+            acc[mi][ni][1] += v.y;
+          }
+      }
 
-      const bool whole = (kb0 == 0 && kb1 == num_kb);
       struct StoreMark {  // first item's results written (any path)
         unsigned long long* tl; bool on;
         __device__ ~StoreMark() { if (on) tl[5] = globaltimer_ns(); }
@@ -390,15 +437,16 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB>::THREADS, 1)
     }
   }
   __syncwarp();
-  __syncthreads();
+  // CK > 1: rank 0's exchange buffer is written by rank 1; neither CTA leaves before both are done
+  if constexpr (CK > 1) cluster_sync(); else __syncthreads();
   if (tl && threadIdx.x == 0) tl[6] = globaltimer_ns();
 }
 
-template <int BM, int BN, int WM, int WN, int KS, int KB = 1>
+template <int BM, int BN, int WM, int WN, int KS, int KB = 1, int CK = 1>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3, const CUtensorMap& tmB3,
                         const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
-  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB>;
-  auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS, KB>;
+  using Cfg = F64Cfg<BM, BN, WM, WN, KS, KB, CK>;
+  auto kern = gemm_f64_kernel<BM, BN, WM, WN, KS, KB, CK>;
   static std::atomic<bool> attr_set[kMaxDevices];  // function attributes are per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -409,15 +457,26 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
     attr_set[dev].store(true);
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.sched.nc, 1, 1);
+  cfg.gridDim = dim3(pl.sched.nc * CK, 1, 1);
   cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (CK > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CK;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (!knob("MM_NO_PDL")) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = knob("MM_NO_PDL") ? 0 : 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA3, tmB3, a, pl.sched);
 }
 
@@ -470,6 +529,9 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   // 32x32 whole tiles: 4 k-blocks per TMA load (the caller drops to 1 unless n, p are 16-multiples)
   pl.kb = (pl.bm == 32 && mode == 0 && (pl.ks == 1 || pl.ks == 2)) ? 4 : 1;
   if (const char* e = knob("MM_F64_KB")) pl.kb = (pl.kb == 4 && atoi(e) == 4) ? 4 : 1;  // tuning knob
+  // at most half a wave of whole 32x32 tiles: split every tile's K over a 2-CTA cluster (knob MM_F64_CK=1 off)
+  pl.ck = (pl.bm == 32 && mode == 0 && 2 * T <= num_sms && pl.ks == 2 && num_kb >= 2) ? 2 : 1;
+  if (const char* e = knob("MM_F64_CK")) pl.ck = (pl.ck == 2 && atoi(e) == 2) ? 2 : 1;
   int group_m = 8;
   if (const char* e = knob("MM_F64_GROUP_M")) group_m = atoi(e) > 0 ? atoi(e) : group_m;  // tuning knob
   pl.sched = sched_build(tiles_m, tiles_n, group_m, num_kb, (int)std::max<int64_t>(1, nc), mode);
@@ -501,12 +563,14 @@ cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     return launch_impl<64, 64, 4, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
   }
   if (pl.kb > 1) {  // 32x32, grouped loads (KB = 4 k-blocks per TMA load)
+    if (pl.ck == 2 && pl.ks == 2) return launch_impl<32, 32, 2, 2, 2, 4, 2>(tmA, tmB, tmA3, tmB3, a, pl, s);
     if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);
     return launch_impl<32, 32, 2, 2, 1, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);
   }
   if (pl.ks == 8) return launch_impl<32, 32, 1, 1, 8>(tmA, tmB, tmA3, tmB3, a, pl, s);   // 8 warps, each 32x32 over 1/8 of K
   if (pl.ks == 44) return launch_impl<32, 32, 2, 2, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);  // 16 warps, 16x16 over 1/4 of K
   if (pl.ks == 4) return launch_impl<32, 32, 1, 1, 4>(tmA, tmB, tmA3, tmB3, a, pl, s);   // 4 warps, each 32x32 over 1/4 of K
+  if (pl.ck == 2 && pl.ks == 2) return launch_impl<32, 32, 2, 2, 2, 1, 2>(tmA, tmB, tmA3, tmB3, a, pl, s);
   if (pl.ks == 2) return launch_impl<32, 32, 2, 2, 2>(tmA, tmB, tmA3, tmB3, a, pl, s);
   return launch_impl<32, 32, 2, 2, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
 }

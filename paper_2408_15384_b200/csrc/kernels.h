@@ -21,6 +21,7 @@ struct GemmArgs {
   int* err;      // device error word (pipeline timeout codes)
   unsigned* sync;  // [0] wave-barrier arrivals, [1] CTAs done (self-resetting)
   int wave_sync;   // align the k-phase of all tiles once per wave (L2 reuse)
+  int pace;        // tcgen05 kernel: k-phase pacing checkpoint every `pace` k-blocks (0: off)
   void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)
@@ -36,6 +37,7 @@ struct F64Plan {
   int bm, bn;       // CTA tile
   int ks;           // k-block groups of consumer warps (small tiles)
   int kb;           // k-blocks per TMA load (small tiles: 3-D slab maps; 1 = 2-D boxes)
+  int ck;           // CTAs per tile along K (2: a cluster splits each tile's K; few small tiles)
   WorkSched sched;  // whole-tile waves + split tail over sched.nc persistent CTAs
   size_t ws_bytes;
   int flag_count;

@@ -268,6 +268,8 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
   int wave_sync = ctx->wave_sync;
   if (const char* e = knob("MM_WAVE_SYNC")) wave_sync = atoi(e);  // tuning knob (0 off, 1 auto, 2 on)
   a.wave_sync = wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (wave_sync > 1);
+  a.pace = 0;
+  if (const char* e = knob("MM_PACE")) a.pace = std::max(0, atoi(e));  // tuning knob (tcgen05 kernel)
 
   CUtensorMap tmA, tmB;
   uint32_t abox[2], bbox[2];
@@ -576,7 +578,7 @@ __attribute__((visibility("default"))) mm_status mm_create(int device, void* wor
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  if (cudaMalloc(&ctx->d_err, 4 * sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, 4 * sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->d_err, 8 * sizeof(int)) != cudaSuccess || cudaMemset(ctx->d_err, 0, 8 * sizeof(int)) != cudaSuccess) {
     cudaSetDevice(prev);
     delete ctx;
     return MM_ERR_RUNTIME;
@@ -690,7 +692,7 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
   if (cudaMemcpy(&h, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "reading the device error word failed");
   if (h != 0) {
-    cudaMemset(ctx->d_err, 0, 4 * sizeof(int));  // error word + wave-barrier counters
+    cudaMemset(ctx->d_err, 0, 8 * sizeof(int));  // error word + wave-barrier / pacing counters
     if (ctx->sk_flags) cudaMemset(ctx->sk_flags, 0, ctx->sk_flag_count * sizeof(unsigned));
     return set_err(ctx, MM_ERR_RUNTIME, "device pipeline wait timed out (code %d)", h);
   }

@@ -56,6 +56,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Store two doubles into another CTA's shared memory (address from mapa_shared).
+__device__ __forceinline__ void st_cluster_d2(uint32_t cluster_addr, double a, double b) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(cluster_addr), "d"(a), "d"(b) : "memory");
+}
 // Arrive on an mbarrier in another CTA of the cluster (address from mapa_shared).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
@@ -151,6 +155,19 @@ __device__ __forceinline__ void soft_wave_wait(unsigned* sync, unsigned target) 
     __nanosleep(32);
     if (globaltimer_ns() - t0 > MMB_SOFT_BARRIER_NS) {
       atomicExch(sync + 2, 1u);
+      return;
+    }
+  }
+}
+// Same, on counter `ctr` with the abandoned flag at `flag` (k-phase pacing checkpoints).
+__device__ __forceinline__ void soft_wait_ctr(const unsigned* ctr, unsigned* flag, unsigned target) {
+  if (ld_acquire_gpu(flag) != 0u || ld_acquire_gpu(ctr) >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu(ctr) < target) {
+    if (ld_acquire_gpu(flag) != 0u) return;
+    __nanosleep(32);
+    if (globaltimer_ns() - t0 > MMB_SOFT_BARRIER_NS) {
+      atomicExch(flag, 1u);
       return;
     }
   }

@@ -30,6 +30,7 @@ KNOBS_F64 = {
     "MM_F64_TILE": [None, "32", "64", "128"],
     "MM_F64_STREAMK": [None, "0", "1"],
     "MM_F64_W8": [None, None, None, "1"],
+    "MM_F64_CK": [None, None, "1"],
 }
 
 

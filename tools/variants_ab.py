@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--flush", action="store_true")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--graph", action="store_true", help="per-product time of 100 products replayed from a CUDA graph")
     args = ap.parse_args()
     dt, shp = args.case.split(":")
     dims = [int(x) for x in shp.split("x")]
@@ -61,6 +62,28 @@ def main():
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
+            if args.graph:
+                st = torch.cuda.Stream()
+                st.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(st):
+                    fn()
+                torch.cuda.current_stream().wait_stream(st)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(100):
+                        fn()
+                g.replay()
+                torch.cuda.synchronize()
+                ts = []
+                for _ in range(args.reps):
+                    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+                    e0.record()
+                    g.replay()
+                    e1.record()
+                    e1.synchronize()
+                    ts.append(e0.elapsed_time(e1) / 100)
+                return statistics.median(ts)
             if flush is not None:
                 ts = []
                 for _ in range(args.reps):
@@ -103,7 +126,8 @@ def main():
     mm.sync_check()
     fl = 2.0 * m * n * p
     lib_ms = statistics.median(res["cublas"])
-    print(f"{args.case} {'flush' if flush is not None else f'{args.window_s}s windows'}: cuBLAS {lib_ms:.4f} ms "
+    mode = "graph x100" if args.graph else ("flush" if flush is not None else f"{args.window_s}s windows")
+    print(f"{args.case} {mode}: cuBLAS {lib_ms:.4f} ms "
           f"({fl / lib_ms / 1e9:.1f} TF)")
     for v in variants:
         ms = statistics.median(res[v])
