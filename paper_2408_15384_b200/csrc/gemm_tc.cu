@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       bool ok = true;
       int t, kb0, kb1;
-      int pace_cp = 0;  // pacing checkpoints passed (MM_PACE)
       // L2 priorities (large operands): the A panels of a raster group are re-read by every
       // wave of the group, the B slabs only within one wave -> keep A, stream B.
       // l2_hint bit 0: A evict_last; bit 1: B evict_first (else evict_normal)
@@ -232,15 +231,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = ((args.debug & 2) ? 0 : tm * Cfg::M_TILE) + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = ((args.debug & 2) ? 0 : tn * Cfg::TILE_N) + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
         for (int kb = kb0; kb < kb1; ++kb) {
-          // k-phase pacing (knob MM_PACE = P): every P k-blocks of a full-wave tile the producer
-          // announces a checkpoint and may run at most one checkpoint ahead of the grid's average,
-          // so neighbouring tiles keep requesting the same A/B slabs at the same time (L2 serves
-          // identical in-flight requests once).  Soft like the wave barrier.
-          if (args.pace && j < sched.W && kb > kb0 && (kb - kb0) % args.pace == 0) {
-            ++pace_cp;
-            red_release_gpu_add(args.sync + 3, 1u);
-            soft_wait_ctr(args.sync + 3, args.sync + 2, (unsigned)(pace_cp - 1) * gridDim.x);
-          }
           const uint64_t te0 = args.trace ? globaltimer_ns() : 0;
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
           if (args.trace) tr_empty += globaltimer_ns() - te0;
@@ -693,12 +683,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   // the last CTA to finish resets the wave-barrier counters (and the abandoned flag) for the next launch
-  if ((args.wave_sync || args.pace) && threadIdx.x == 0) {
+  if (args.wave_sync && threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(args.sync + 1, 1u) == gridDim.x - 1) {
       atomicExch(args.sync, 0u);
       atomicExch(args.sync + 2, 0u);
-      atomicExch(args.sync + 3, 0u);
       atomicExch(args.sync + 1, 0u);
     }
   }

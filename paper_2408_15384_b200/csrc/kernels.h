@@ -21,7 +21,6 @@ struct GemmArgs {
   int* err;      // device error word (pipeline timeout codes)
   unsigned* sync;  // [0] wave-barrier arrivals, [1] CTAs done (self-resetting)
   int wave_sync;   // align the k-phase of all tiles once per wave (L2 reuse)
-  int pace;        // tcgen05 kernel: k-phase pacing checkpoint every `pace` k-blocks (0: off)
   void* ws;         // FP64 stream-K partial tiles (grid × BM × BN doubles)
   unsigned* flags;  // stream-K per-tile arrival counters (zero between launches)
   int c_tma;        // tcgen05 kernel: C written by TMA stores (C base and pitch 16-B aligned)

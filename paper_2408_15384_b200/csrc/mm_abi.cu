@@ -268,8 +268,6 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
   int wave_sync = ctx->wave_sync;
   if (const char* e = knob("MM_WAVE_SYNC")) wave_sync = atoi(e);  // tuning knob (0 off, 1 auto, 2 on)
   a.wave_sync = wave_sync == 1 ? (operand_bytes > 96.0 * (1 << 20)) : (wave_sync > 1);
-  a.pace = 0;
-  if (const char* e = knob("MM_PACE")) a.pace = std::max(0, atoi(e));  // tuning knob (tcgen05 kernel)
 
   CUtensorMap tmA, tmB;
   uint32_t abox[2], bbox[2];

@@ -159,19 +159,6 @@ __device__ __forceinline__ void soft_wave_wait(unsigned* sync, unsigned target) 
     }
   }
 }
-// Same, on counter `ctr` with the abandoned flag at `flag` (k-phase pacing checkpoints).
-__device__ __forceinline__ void soft_wait_ctr(const unsigned* ctr, unsigned* flag, unsigned target) {
-  if (ld_acquire_gpu(flag) != 0u || ld_acquire_gpu(ctr) >= target) return;
-  const uint64_t t0 = globaltimer_ns();
-  while (ld_acquire_gpu(ctr) < target) {
-    if (ld_acquire_gpu(flag) != 0u) return;
-    __nanosleep(32);
-    if (globaltimer_ns() - t0 > MMB_SOFT_BARRIER_NS) {
-      atomicExch(flag, 1u);
-      return;
-    }
-  }
-}
 __device__ __forceinline__ unsigned atomic_add_acq_rel_gpu(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
