@@ -441,6 +441,54 @@ def per_config_table(mm, peaks, k6=None):
     return out
 
 
+def scaling_projection(mm, A, B, ms_full, steps):
+    """Single-GPU projection of the sharded configs (context only; the driver's multi-GPU runs are
+    the measurement): in the resident row-block regime every rank runs one row block of C4 with no
+    data-path collective, so a rank's time on this GPU projects T_G; SUMMA ranks run their local
+    C5 block products (k-panels of 2048, beta = 1) — communication (panel broadcasts ~4.3 GB per
+    rank, ~1 % of compute at G <= 8 over 900 GB/s NVLink) is not included, and the block
+    product is timed as one call (the plan splits it into 2048-wide k-panels with beta = 1)."""
+    import torch
+    out = {"what": "one GPU running one rank's share of the work; projected E_G = T_1 / (G * T_G)"}
+    M_ = A.shape[0]
+    rows = {}
+    for G in (2, 4, 8):
+        r = -(-M_ // G)
+        Ar = A[:r].contiguous()
+        Cr = torch.empty(r, B.shape[1], dtype=torch.float32, device="cuda")
+        t = device_time_steps(lambda: mm.gemm(Ar, B, out=Cr), max(steps, 10), 3)
+        rows[G] = {"block_rows": r, "ms": round(t, 4), "projected_resident_efficiency": round(ms_full / (G * t), 4)}
+        del Ar, Cr
+    out["C4_row_block"] = rows
+    out["C4_row_block_note"] = ("T_1 = the headline ms_per_step; same back-to-back burst method; the G=8 block "
+                                "(2048 rows) splits its 34-tile last round in K halves")
+    from synthgen import gpu as sgg
+    N = 32768
+    try:
+        A5 = sgg.uniform_f64(4, 1, N, N)
+        B5 = sgg.uniform_f64(4, 2, N, N)
+
+        def summa_local(pr, pc):
+            ar, bc = -(-N // pr), -(-N // pc)
+            Ab, Bb = A5[:ar].contiguous(), B5[:, :bc].contiguous()
+            Cb = torch.empty(ar, bc, dtype=torch.float64, device="cuda")
+            # the whole local block product in one call (the plan runs it as 16 k-panels with beta = 1)
+            t = device_time_steps(lambda: mm.gemm(Ab, Bb, out=Cb), 1, 1)
+            del Ab, Bb, Cb
+            return t
+        t1 = device_time_steps(lambda: mm.gemm(A5, B5), 1, 1)
+        summa = {"T1_ms": round(t1, 1)}
+        for G, (pr, pc) in ((2, (1, 2)), (4, (2, 2)), (8, (2, 4))):
+            t = summa_local(pr, pc)
+            summa[f"G{G}_{pr}x{pc}"] = {"local_product_ms": round(t, 1), "projected_efficiency": round(t1 / (G * t), 4)}
+        out["C5_summa_local"] = summa
+        del A5, B5
+        torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001
+        out["C5_summa_local"] = {"error": str(e)[:200]}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (oracle/, as it stands) on this host's physical cores
     (OpenMP threads bound to cores), on bounded row samples of the C4 workload (rank 0 only)."""
@@ -687,8 +735,14 @@ def main():
         }
 
     per_config = None
+    projection = None
     if rank == 0 and not args.no_per_config:
         per_config = per_config_table(mm, peaks, k6)
+        if world == 1:
+            try:
+                projection = scaling_projection(mm, A, B, ms, args.steps)
+            except Exception as e:  # noqa: BLE001
+                projection = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -715,6 +769,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "sustained": sustained, "k6_peaks": k6,
             "with_comm": with_comm, "library_baseline": library, "per_config": per_config,
+            "scaling_projection_single_gpu": projection,
             "protocol": protocol,
             "fraction_of_dense_peak": {"vs_measured_burst": round(value / world / peaks["bf16_tflops"], 4),
                                        "vs_measured_sustained": round(value / world / peaks["bf16_tflops_sustained"], 4),
