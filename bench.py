@@ -109,10 +109,12 @@ CONFIG_SHAPES = {"C1": ("f64", 256, 256, 256, 0), "C2": ("f64", 2000, 1500, 1750
                  "C4": ("bf16", 16384, 16384, 16384, 3), "C5": ("f64", 32768, 32768, 32768, 4)}
 
 
-def oracle_worker(mode, threads):
-    """`bench.py --oracle-worker MODE --threads T`: the CPU oracle (oracle/, as it stands) timed in a
-    fresh process that loads nothing but numpy, oracle/ and synthgen/ (no torch, no CUDA context),
-    with OpenMP threads bound to cores.  Prints one JSON line."""
+def oracle_worker(mode, threads, only=None):
+    """`bench.py --oracle-worker MODE --threads T [--config Cx]`: the CPU oracle (oracle/, as it
+    stands) timed in a fresh process that loads nothing but numpy, oracle/ and synthgen/ (no torch,
+    no CUDA context), with OpenMP threads bound to cores.  Prints one JSON line.  One config per
+    process: after three FP64 C2 products the same process ran the BF16 C4 rows 2.3-3x slower
+    (reproduced on the build host), so every config gets a clean process."""
     import ctypes
     import oracle
     import synthgen as sg
@@ -120,6 +122,8 @@ def oracle_worker(mode, threads):
     usable = len(os.sched_getaffinity(0))
     out = {"mode": mode, "threads": threads}
     for cfg, spec in ORACLE_WORK[mode].items():
+        if only and cfg != only:
+            continue
         dt, m, n, p, seed = CONFIG_SHAPES[cfg]
         rows = m if spec == 0 else (2 * threads if spec == "2T" else threads if spec == "T" else int(spec))
         gomp.omp_set_num_threads(usable)  # input generation is not timed: all CPUs
@@ -136,11 +140,10 @@ def oracle_worker(mode, threads):
         assert oracle.max_threads() == threads
         fn()  # warm-up (thread pool, first touch of the output): the reference arm also warms up
         reps = 3 if 2.0 * rows * n * p < 1e9 else 2
-        best = float("inf")
+        t0 = time.perf_counter()
         for _ in range(reps):
-            t0 = time.perf_counter()
             fn()
-            best = min(best, time.perf_counter() - t0)
+        best = (time.perf_counter() - t0) / reps  # mean after a warm-up, as the reference arm reports
         flops = 2.0 * rows * n * p
         full = 2.0 * m * n * p
         out[cfg] = {"dtype": dt, "shape": [m, n, p], "rows_timed": rows, "seconds": round(best, 4),
@@ -153,19 +156,22 @@ def oracle_worker(mode, threads):
 
 
 def oracle_baseline(modes=("serial", "parallel")):
-    """Run oracle_worker in clean subprocesses (serial, and all physical cores) -> dict."""
+    """Run oracle_worker in clean subprocesses (one per mode and config; serial, and all physical
+    cores) -> dict."""
     cpu = host_cpu_info()
     res = {"host": cpu}
     for mode in modes:
         T = 1 if mode == "serial" else cpu["parallel_threads"]
         env = dict(os.environ, OMP_NUM_THREADS=str(T), OMP_PROC_BIND="close", OMP_PLACES="cores")
-        try:
-            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker", mode, "--threads", str(T)],
-                               capture_output=True, text=True, env=env, timeout=900)
-            lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
-            res[mode] = json.loads(lines[-1]) if lines else {"error": r.stderr[-300:]}
-        except subprocess.TimeoutExpired:
-            res[mode] = {"error": "timeout"}
+        res[mode] = {"mode": mode, "threads": T}
+        for cfg in ORACLE_WORK[mode]:
+            try:
+                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker", mode, "--threads", str(T),
+                                    "--config", cfg], capture_output=True, text=True, env=env, timeout=600)
+                lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+                res[mode][cfg] = json.loads(lines[-1]).get(cfg) if lines else {"error": r.stderr[-300:]}
+            except subprocess.TimeoutExpired:
+                res[mode][cfg] = {"error": "timeout"}
     return res
 
 
@@ -540,9 +546,10 @@ def main():
     ap.add_argument("--no-k6", action="store_true")
     ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--threads", type=int, default=1, help=argparse.SUPPRESS)
+    ap.add_argument("--config", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.oracle_worker:
-        return oracle_worker(args.oracle_worker, args.threads)
+        return oracle_worker(args.oracle_worker, args.threads, args.config)
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
