@@ -81,6 +81,11 @@ struct TcCfg {
   // a_major [15] = K, b_major [16] = MN, N>>3 at [17,23), M>>4 at [24,29).
   static constexpr uint32_t IDESC = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                                     ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(M_MMA >> 4) << 24);
+  // N-half tail items (sched.nhalf): the pair's MMA is N = 128, each CTA stages 64 columns of B
+  // (bf16: one 128-B box of the regular map; int8: a 64-B box through a SWIZZLE_64B map)
+  static constexpr uint32_t IDESC_H = ((I8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                                      ((uint32_t)((kBN / 2) >> 3) << 17) | ((uint32_t)(M_MMA >> 4) << 24);
+  static constexpr int HB_BYTES = BK * 64 * ESZ;  // one CTA's 64 columns of B per stage
 };
 
 __device__ __forceinline__ void store_row32(uint32_t* __restrict__ C, int64_t ldc, int64_t row, int64_t col0,
@@ -139,7 +144,8 @@ __device__ __forceinline__ void add32(uint32_t (&v)[32], const uint4* __restrict
 template <bool I8, int CG, int NT, int MC, int KA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, GemmArgs args, WorkSched sched) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmBh, GemmArgs args,
+                   WorkSched sched) {
   using Cfg = TcCfg<I8, CG, NT, MC, KA>;
   const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
   // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
@@ -227,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (args.trace) tr_barrier += globaltimer_ns() - tb0;
         int tm, tn;
         sched.tile_coords(t, tm, tn);
+        const int hf = sched.half_of(cl, j);  // N half of a tail tile, or -1
         // (diagnostics, MM_DEBUG bit 1: every tile reads the first tile's operands -> L2 hits only)
         const int m0 = ((args.debug & 2) ? 0 : tm * Cfg::M_TILE) + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = ((args.debug & 2) ? 0 : tn * Cfg::TILE_N) + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
@@ -272,6 +279,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d_pair_mc(sb + rb * Cfg::BOX_BYTES + pair * Cfg::B_PART, &tmB, leader_full,
                                   n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN,
                                   k0 + (int)pair * Cfg::BKB, mask);
+          } else if (NT == 1 && hf >= 0) {
+            // N-half tail item: this CTA's 128 rows of A, and its 64 of the half's 128 columns of B
+            const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
+            if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * (Cfg::A_BYTES + Cfg::HB_BYTES));
+#pragma unroll
+            for (int a = 0; a < KA; ++a)
+              tma_load_2d_pair(sa + a * Cfg::A_ATOM, &tmA, leader_full, k0 + a * Cfg::BKA, m0);
+            tma_load_2d_pair(sb, &tmBh, leader_full, tn * Cfg::TILE_N + hf * (kBN / 2) + (int)rank * (kBN / 4), k0);
           } else {
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
@@ -328,6 +343,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       };
+      // MMAs of one k-block of an N-half tail item (pair N = 128) into accumulator `d_tmem`
+      auto issue_half = [&](uint32_t d_tmem, int stg, bool first_kb) {
+        const uint32_t sa = sA + stg * Cfg::A_BYTES;
+        const uint32_t sb = sB + stg * Cfg::B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
+          const uint64_t adesc = umma_desc_sw128(sa + (kk / Cfg::KPA) * Cfg::A_ATOM + (kk % Cfg::KPA) * 32, 16, 1024);
+          // B: MN-major, one 64-column block per CTA: bf16 rows of 128 B (SW128), int8 rows of 64 B (SW64)
+          const uint64_t bdesc = I8 ? umma_desc_sw64(sb + kk * Cfg::UK * 64, Cfg::HB_BYTES, 512)
+                                    : umma_desc_sw128(sb + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
+          if (lane == 0) tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC_H, (!first_kb || kk != 0) ? 1u : 0u);
+        }
+      };
       auto wait_tempty = [&](int a, uint32_t parity) {
         const uint64_t tt0 = args.trace ? globaltimer_ns() : 0;
         const bool r = CG == 2 ? mbar_wait_cluster(tempty_bar(a), parity, err, 2) : mbar_wait(tempty_bar(a), parity, err, 2);
@@ -376,10 +404,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           if (!wait_tempty(acc, (use & 1u) ^ 1u)) { ok = false; break; }
         }
+        const bool half_item = NT == 1 && CG == 2 && MC == 1 && sched.half_of(cl, j) >= 0;
         for (; kb < kb1; ++kb) {
           if (!wait_full(stage, phase)) { ok = false; break; }
           if (tl && lane == 0 && tl_first && j < 8) { tl[4 * j] = globaltimer_ns(); tl_first = false; }
-          issue(d_tmem, stage, kb == kb0, 0, NT);
+          if (half_item) issue_half(d_tmem, stage, kb == kb0);
+          else issue(d_tmem, stage, kb == kb0, 0, NT);
           // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
           // in the other pair, whose producers multicast into this pair's slots
           if (lane == 0) tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
@@ -541,6 +571,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(t_row + c * 32, v);
           tmem_ld_wait();
           emit(v, row_base, col_t + c * 32, true);
+        }
+      } else if (NT == 1 && sched.half_of(cl, j) >= 0) {
+        // N-half tail item: 128 columns (chunks 0..3) starting at the half's first column
+        const int64_t col_h = col_t + (int64_t)sched.half_of(cl, j) * (kBN / 2);
+#pragma unroll 1
+        for (int c = h; c < NCH / 2; c += 2) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + c * 32, v);
+          tmem_ld_wait();
+          emit(v, row_base, col_h + c * 32);
         }
       } else if (whole) {
         // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
@@ -735,7 +775,19 @@ WorkSched make_sched(bool i8, int cg, int nt, int mc, int64_t M, int64_t N, int6
   // 8.2 -> 10.8 us)
   if (tail > 0 && mc == 1 && 2 * tail <= nc && K >= (i8 ? 4608 : 2304))
     mode = c_tma ? 3 : ((!i8 && nt == 1 && num_kb >= 8) ? 2 : 0);
+  // Round 2: the tail tiles of 256-wide pair tiles as two N halves on two clusters (pair MMA N = 128,
+  // whole K each): no partial sums and no reduce-add, so it beats whole tiles at every K and the K
+  // halves below K = 3072 (BF16) / 6144 (INT8) — measured at 4096 x K x 4096 (34-tile tail):
+  // INT8 K = 2048 / 3072 / 4096 / 5120: 0.0389 / 0.0482 / 0.0584 / 0.0702 ms vs K halves 0.0461 /
+  // 0.0543 / 0.0615 / 0.0707 and whole tiles 0.0399 / 0.0502 / 0.0604 / 0.0707; BF16 K = 768 / 1536
+  // / 2048 / 2560: 33.8 / 50.2 / 62.5 / 72.7 us vs 42.0 / 56.4 / 64.5 / 74.8 (K halves); from
+  // BF16 K = 4096 / INT8 K = 8192 the K halves win (profiles/sweep_tail_r2o.txt).  Without a
+  // reduce-add (C not TMA-storable, or in a peer's memory) N halves replace the landing split.
+  if (tail > 0 && mc == 1 && cg == 2 && nt == 1 && 2 * tail <= nc &&
+      (K < (i8 ? 6144 : 3072) || !c_tma))
+    mode = 4;
   if (const char* e = knob("MM_STREAMK")) mode = tail > 0 ? atoi(e) : 0;  // tuning knob
+  if (mode == 4 && (nt != 1 || cg != 2 || mc != 1 || 2 * tail > nc)) mode = 0;  // N halves: 256-wide pair tiles
   if (knob("MM_ONE_TILE")) return sched_build(tiles_m, tiles_n, group_m, num_kb, (int)T, 0);  // (A/B knob: one tile per cluster, non-persistent)
   if (mc != 1) mode = 0;                // (cluster-pair multicast: whole tiles only)
   if (mode == 2 && (nt != 1 || 2 * tail > nc)) mode = 1;  // landing: 256-wide tiles, one partner per tile
@@ -783,8 +835,8 @@ cudaError_t launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, int n
 }
 
 template <bool I8, int CG, int NT, int MC, int KA = 1>
-cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& a,
-                        int num_sms, cudaStream_t s) {
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const CUtensorMap& tmBh,
+                        const GemmArgs& a, int num_sms, cudaStream_t s) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[2];
   int max_cl = 0;
@@ -793,7 +845,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   const WorkSched sched = make_sched(I8, CG, NT, MC, a.M, a.N, a.K, num_sms, max_cl, KA, a.c_tma != 0 && !a.no_reduce);
   cfg.gridDim = dim3(sched.nc * CG * MC, 1, 1);
   cfg.stream = s;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, a, sched);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<I8, CG, NT, MC, KA>, tmA, tmB, tmC, tmBh, a, sched);
 }
 
 template <bool I8, int CG, int NT, int MC, int KA = 1>
@@ -843,28 +895,29 @@ void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N
 }
 
 cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s) {
+                           const CUtensorMap& tmC, const CUtensorMap& tmBh, const GemmArgs& a, int num_sms,
+                           cudaStream_t s) {
   if (cg == 1)
-    return i8 ? launch_impl<true, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s)
-              : launch_impl<false, 1, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+    return i8 ? launch_impl<true, 1, 1, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+              : launch_impl<false, 1, 1, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s);
   if (mc == 2 && nt == 1 && a.ka == 2)
-    return i8 ? launch_impl<true, 2, 1, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
-              : launch_impl<false, 2, 1, 2, 2>(tmA, tmB, tmC, a, num_sms, s);
+    return i8 ? launch_impl<true, 2, 1, 2, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+              : launch_impl<false, 2, 1, 2, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s);
   if (mc == 2) {
     if (i8)
-      return nt == 2 ? launch_impl<true, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
-                     : launch_impl<true, 2, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
-    return nt == 2 ? launch_impl<false, 2, 2, 2>(tmA, tmB, tmC, a, num_sms, s)
-                   : launch_impl<false, 2, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
+      return nt == 2 ? launch_impl<true, 2, 2, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+                     : launch_impl<true, 2, 1, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s);
+    return nt == 2 ? launch_impl<false, 2, 2, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+                   : launch_impl<false, 2, 1, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s);
   }
   if (nt == 1 && a.ka == 2)
-    return i8 ? launch_impl<true, 2, 1, 1, 2>(tmA, tmB, tmC, a, num_sms, s)
-              : launch_impl<false, 2, 1, 1, 2>(tmA, tmB, tmC, a, num_sms, s);
+    return i8 ? launch_impl<true, 2, 1, 1, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+              : launch_impl<false, 2, 1, 1, 2>(tmA, tmB, tmC, tmBh, a, num_sms, s);
   if (i8)
-    return nt == 2 ? launch_impl<true, 2, 2, 1>(tmA, tmB, tmC, a, num_sms, s)
-                   : launch_impl<true, 2, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
-  return nt == 2 ? launch_impl<false, 2, 2, 1>(tmA, tmB, tmC, a, num_sms, s)
-                 : launch_impl<false, 2, 1, 1>(tmA, tmB, tmC, a, num_sms, s);
+    return nt == 2 ? launch_impl<true, 2, 2, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+                   : launch_impl<true, 2, 1, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s);
+  return nt == 2 ? launch_impl<false, 2, 2, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s)
+                 : launch_impl<false, 2, 1, 1>(tmA, tmB, tmC, tmBh, a, num_sms, s);
 }
 
 }  // namespace mmb

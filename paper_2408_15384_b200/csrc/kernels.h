@@ -47,8 +47,10 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms);
 // tmA: dims {K, M} box {128 B of K, 128 rows}; tmB: dims {N, K} box {128 B of N, BK rows}; both SWIZZLE_128B.
 // nt: accumulators of N=256 per tile (1: 256-wide tiles, TMEM double-buffered; 2: 512-wide tiles, CG=2 only).
 // mc: CTA pairs per cluster sharing B (2: clusters of 4 CTAs, 512-row tiles, B slabs multicast; CG=2 only).
+// tmBh: B for N-half tail items (sched.nhalf): int8 — box {64 columns, BK rows}, SWIZZLE_64B; bf16 — tmB.
 cudaError_t launch_gemm_tc(bool i8, int cg, int nt, int mc, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                           const CUtensorMap& tmC, const GemmArgs& a, int num_sms, cudaStream_t s);
+                           const CUtensorMap& tmC, const CUtensorMap& tmBh, const GemmArgs& a, int num_sms,
+                           cudaStream_t s);
 // Workspace (stream-K partial slabs) and per-tile counters the launch will use.
 void tc_plan_needs(bool i8, int cg, int nt, int mc, int ka, int64_t M, int64_t N, int64_t K, int num_sms,
                    size_t* ws_bytes, size_t* flag_count);

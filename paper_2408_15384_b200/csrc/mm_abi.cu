@@ -93,9 +93,9 @@ void map_cache_put(mm_ctx* ctx, const uint64_t (&key)[8], const CUtensorMap& m) 
 
 // Row-major rows×cols matrix with pitch `ld` elements → 2-D tensor map {cols, rows}.
 mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_t esz, const void* ptr, int64_t rows,
-                    int64_t cols, int64_t ld, const uint32_t box[2], const char* what) {
+                    int64_t cols, int64_t ld, const uint32_t box[2], const char* what, int swizzle_bytes = 128) {
   const uint64_t key[8] = {2, (uint64_t)(uintptr_t)ptr, (uint64_t)rows, (uint64_t)cols, (uint64_t)ld,
-                           ((uint64_t)box[0] << 32) | box[1], ((uint64_t)dt << 32) | (uint64_t)esz, 128};
+                           ((uint64_t)box[0] << 32) | box[1], ((uint64_t)dt << 32) | (uint64_t)esz, (uint64_t)swizzle_bytes};
   if (map_cache_get(ctx, key, map)) return MM_OK;
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_err(ctx, MM_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -104,8 +104,8 @@ mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_
   cuuint32_t boxd[2] = {box[0], box[1]};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
                    (long long)rows, (long long)cols, (long long)ld, (int)r);
@@ -420,7 +420,15 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
                      cbox, "C");
       if (st != MM_OK) return st;
     }
-    e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, a, num_sms, s);
+    // B for N-half tail items: bf16 — the same map (a 64-column box is 128 B); int8 — 64-column
+    // (64-B) boxes, 64-byte swizzle
+    CUtensorMap tmBh = tmB;
+    if (i8 && cg == 2 && nt == 1 && mc == 1) {
+      const uint32_t hbox[2] = {64, bbox[1]};
+      st = encode_2d(ctx, &tmBh, dt, esz, Buse, n, p, padB ? ldB2 : ldb, hbox, "B (64-column boxes)", 64);
+      if (st != MM_OK) return st;
+    }
+    e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, tmBh, a, num_sms, s);
     trace_nt = nt;
     trace_mc = mc;
     if (trace) trace_maxcl = max_clusters(i8, cg, nt, mc, a.ka, num_sms);

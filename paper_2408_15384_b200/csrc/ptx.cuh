@@ -397,6 +397,17 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t start, uint32_t lbo
   return d;
 }
 
+// Same descriptor with a 64-byte swizzle (layout type 4): MN-major operands whose rows are 64 B.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t start, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((start >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+
 // ------------------------------------------------------------------ FP64 DMMA
 // D(8×8) += A(8×4, row) · B(4×8, col): thread t holds A[t/4][t%4], B[t%4][t/4],
 // C/D[t/4][2(t%4)+{0,1}].  Lowers to SASS DMMA.8x8x4 on sm_100a.

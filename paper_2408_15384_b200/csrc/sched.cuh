@@ -23,6 +23,7 @@ struct WorkSched {
   int ntc;   // clusters taking part in the stream-K tail (0 = no tail)
   int land;  // tail tiles split in exact halves: the last half lands the other's slab in its idle stage ring
   int red;   // tail tiles split in exact halves, both adding into C (zeroed first) by TMA reduce-add stores
+  int nhalf; // tail tiles split in N halves (whole K each): cluster c < ntc takes half c & 1 of tail tile c / 2
   int64_t TI;  // tail iterations = tail tiles * num_kb
 
   __device__ __forceinline__ void tile_coords(int t, int& tm, int& tn) const {
@@ -41,6 +42,8 @@ struct WorkSched {
     while (c > 0 && tstart(c) > it) --c;
     return c;
   }
+  // N half of item j of cluster c (tail mode 4), or -1 for a whole-width item
+  __device__ __forceinline__ int half_of(int c, int j) const { return (nhalf && j == W && c < ntc) ? (c & 1) : -1; }
   // j-th work item of cluster c: tile t, k-blocks [kb0, kb1). Returns false past the end.
   __device__ __forceinline__ bool item(int c, int j, int& t, int& kb0, int& kb1) const {
     if (j < W) {
@@ -50,6 +53,13 @@ struct WorkSched {
       return t < tiles_m * tiles_n;
     }
     if (c >= ntc) return false;
+    if (nhalf) {
+      if (j != W) return false;
+      t = W * nc + c / 2;
+      kb0 = 0;
+      kb1 = num_kb;
+      return true;
+    }
     int64_t it = tstart(c);
     const int64_t end = tstart(c + 1);
     for (int s = 0; it < end; ++s) {
@@ -73,7 +83,9 @@ struct WorkSched {
 //   tail_mode 1: the tiles of the last partial wave split evenly over the clusters
 //                (>= min_seg k-blocks per segment, <= 4 segments per tile);
 //   tail_mode 2: the tail tiles split in exact halves (needs 2*tail <= nc);
-//   tail_mode 3: the same halves, both added into C by TMA reduce-add (no partial slabs).
+//   tail_mode 3: the same halves, both added into C by TMA reduce-add (no partial slabs);
+//   tail_mode 4: the tail tiles split in N halves, each with its whole K (needs 2*tail <= nc):
+//                no partial sums at all, twice the clusters on the last round.
 inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, int nc, int tail_mode, int min_seg = 4) {
   WorkSched s;
   s.tiles_m = tiles_m;
@@ -87,6 +99,7 @@ inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, 
   s.TI = tail * num_kb;
   s.land = 0;
   s.red = 0;
+  s.nhalf = 0;
   if (tail == 0 || tail_mode == 0 || (tail_mode >= 2 && 2 * tail > s.nc)) {
     s.W = (int)((T + s.nc - 1) / s.nc);
     s.ntc = 0;
@@ -95,6 +108,8 @@ inline WorkSched sched_build(int tiles_m, int tiles_n, int group_m, int num_kb, 
     s.ntc = (int)(2 * tail);  // exact halves: two parts per tile
     s.land = tail_mode == 2;
     s.red = tail_mode == 3;
+    s.nhalf = tail_mode == 4;
+    if (s.nhalf) s.TI = 0;
   } else {
     int64_t ntc = s.nc < tail * 4 ? s.nc : tail * 4;
     const int64_t cap = s.TI / (min_seg < 1 ? 1 : min_seg);

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 N_CASES = 160
 KNOBS_TC = {
-    "MM_STREAMK": [None, "0", "1", "2", "3"],
+    "MM_STREAMK": [None, "0", "1", "2", "3", "4"],
     "MM_NT": [None, "1", "2"],
     "MM_KA": [None, "1"],
     "MM_FORCE_CG": [None, "1", "2"],

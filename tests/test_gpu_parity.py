@@ -737,3 +737,51 @@ def test_config4_fp64_32768_sampled(mm):
     check("f64", Ccol, Cc, Dc, exact=False)
     g = json.load(open(os.path.join(GOLDEN, "survey_c6.json")))["C5"]
     assert Crow[0, 0] == pytest.approx(g["C00"], abs=1e-12 * g["D00"])
+
+
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+def test_n_half_tail(mm, dt):
+    """Tail mode 4: the partial last round's 256-wide pair tiles run as two N-halves on two
+    clusters (pair MMA N = 128, whole K; int8 B through a SWIZZLE_64B map), no partial sums:
+    bit-exact on exact-integer inputs, incl. ragged edges where a half lies outside C, and
+    nothing written outside C (guard bands)."""
+    os.environ["MM_STREAMK"] = "4"
+    try:
+        K = 255 if dt == "i8" else 9
+        out = torch.float32 if dt == "bf16" else torch.int32
+        for (m, n, p) in [(4096, 4096, 4096), (2560, 768, 2560), (2400, 1000, 2700), (4096, 512, 4096),
+                          (1100, 2048, 1700), (2048, 4096, 2176)]:
+            A, B = gen(dt, "exact", 53, m, n, p, K)
+            Cref, _ = ref(dt, A, B)
+            guard = 4096
+            buf = torch.full((guard + m * p + guard,), -7, dtype=out, device="cuda")
+            C = buf[guard:guard + m * p].view(m, p)
+            Ad, Bd = to_dev(A, dt), to_dev(B, dt)
+            for _ in range(3):
+                mm.gemm(Ad, Bd, out=C)
+            mm.sync_check()
+            h = buf.cpu().numpy()
+            assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), (m, n, p)
+            assert np.array_equal(C.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), (m, n, p)
+    finally:
+        os.environ.pop("MM_STREAMK", None)
+
+
+@pytest.mark.parametrize("dt", ["i8", "bf16"])
+def test_n_half_tail_same_bits_as_whole_tiles(mm, dt):
+    """N halves keep each element's K summation exactly as in a whole tile (only N is split), so
+    random-valued results equal the whole-tile schedule bit for bit (R17: no K split)."""
+    m, n, p = 4096, 2048, 4096
+    A, B = gen(dt, "random", 54, m, n, p)
+    Ad, Bd = to_dev(A, dt), to_dev(B, dt)
+    outs = {}
+    for mode in ("0", "4"):
+        os.environ["MM_STREAMK"] = mode
+        try:
+            outs[mode] = mm.gemm(Ad, Bd)
+            mm.sync_check()
+        finally:
+            os.environ.pop("MM_STREAMK", None)
+    assert torch.equal(outs["0"], outs["4"])
+    Cref, D = ref(dt, A[:64], B)
+    check(dt, outs["4"][:64].cpu().numpy(), Cref, D, exact=False)
