@@ -124,6 +124,10 @@ const char* mm_last_error(const mm_ctx* ctx);
  *   onto layer 0 (NCCL reduce); other layers' C_local hold partial sums.
  *   SUMMA layouts are implemented for MM_F64 (they accumulate with β = 1).
  *
+ * Mismatched arguments across ranks are a usage error: the diagnostic build (and the release
+ * library with MM_CHECK_COLLECTIVE=1, at the cost of one all-reduce and a stream synchronisation)
+ * checks them with an all-reduce of their hash and returns MM_ERR_USAGE on every rank.
+ *
  * nccl_comm is an ncclComm_t spanning exactly the G ranks (e.g. torch's
  * ProcessGroupNCCL._comm_ptr()).  The library resolves NCCL symbols at run
  * time from the libnccl.so.2 already loaded in the process.

@@ -370,6 +370,33 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
   int G = 0, r = 0;
   NCCL_CHECK(ctx, api.CommCount(comm, &G));
   NCCL_CHECK(ctx, api.CommUserRank(comm, &r));
+  // Collective contract (include/mm.h): every rank passes the same (m, n, p, dtype, layout, grid,
+  // flags, root).  Checked with one all-reduce of a hash and its negation (MAX of both equals the
+  // hash on every rank iff all hashes agree) in the diagnostic build, or with MM_CHECK_COLLECTIVE=1
+  // (it synchronises the stream, so it is off by default in the release library).
+  bool check = knob("MM_CHECK_COLLECTIVE") != nullptr;
+#ifdef MM_DIAG
+  check = true;
+#endif
+  if (check) {
+    uint64_t hsh = 1469598103934665603ull;
+    const int64_t words[9] = {m, n, p, (int64_t)dtype, (int64_t)layout, grid_rows, grid_cols, (int64_t)flags, root};
+    for (int64_t w : words) hsh = (hsh ^ (uint64_t)w) * 1099511628211ull;
+    const int64_t h = (int64_t)(hsh >> 2);  // (positive)
+    int64_t pair[2] = {h, -h};
+    if (!ctx->bar_buf && cudaMalloc(&ctx->bar_buf, 16) != cudaSuccess)
+      return set_err(ctx, MM_ERR_WORKSPACE, "barrier buffer allocation failed");
+    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(ctx->bar_buf, pair, sizeof pair, cudaMemcpyHostToDevice, s0) != cudaSuccess)
+      return set_err(ctx, MM_ERR_RUNTIME, "collective check staging failed");
+    NCCL_CHECK(ctx, api.AllReduce(ctx->bar_buf, ctx->bar_buf, 2, ncclInt64, ncclMax, comm, s0));
+    if (cudaMemcpyAsync(pair, ctx->bar_buf, sizeof pair, cudaMemcpyDeviceToHost, s0) != cudaSuccess ||
+        cudaStreamSynchronize(s0) != cudaSuccess)
+      return set_err(ctx, MM_ERR_RUNTIME, "collective check failed");
+    if (pair[0] != h || pair[1] != -h)
+      return set_err(ctx, MM_ERR_USAGE, "rank %d: mm_gemm_sharded arguments differ across the %d ranks "
+                     "(m, n, p, dtype, layout, grid, flags and root must match)", r, G);
+  }
   // argument errors with messages (mm_shard_plan applies the same rules)
   if (layout == MM_ROW_BLOCK) {
     if (root < 0 || root >= G) return set_err(ctx, MM_ERR_USAGE, "root %d outside [0, %d)", root, G);

@@ -138,3 +138,20 @@ def test_summa25d_world1_fp64(pg):
                     layout=mm.MM_SUMMA_25D, grid=(1, 1), flags=mm.MM_REPLICATE)
     mm.sync_check()
     assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
+
+
+def test_collective_argument_check(pg):
+    """MM_CHECK_COLLECTIVE=1: the hash all-reduce runs (world size 1: always consistent) and the
+    product is unchanged."""
+    import paper_2408_15384_b200 as mm
+    m, n, p = 300, 200, 260
+    A, B = sg.exact_f64(36, 1, 2049, m, n), sg.exact_f64(36, 2, 2049, n, p)
+    C = torch.empty(m, p, dtype=torch.float64, device="cuda")
+    os.environ["MM_CHECK_COLLECTIVE"] = "1"
+    try:
+        mm.gemm_sharded(m, n, p, torch.float64, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), C,
+                        layout=mm.MM_ROW_BLOCK)
+        mm.sync_check()
+    finally:
+        os.environ.pop("MM_CHECK_COLLECTIVE", None)
+    assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
