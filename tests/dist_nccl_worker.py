@@ -105,6 +105,26 @@ def row_block_small(G, r, checks):
             checks.append({"what": f"row-block {dt} {m}x{n}x{p} flags={flags} root={root}", "ok": allreduce_ok(ok)})
 
 
+def collective_check(G, r, checks):
+    """MM_CHECK_COLLECTIVE=1: matching arguments pass; a rank-dependent m is MM_ERR_USAGE on every rank."""
+    os.environ["MM_CHECK_COLLECTIVE"] = "1"
+    try:
+        m, n, p = 64 + (r if G > 1 else 0), 32, 48
+        A = torch.ones(m, n, dtype=torch.float64, device="cuda")
+        B = torch.ones(n, p, dtype=torch.float64, device="cuda")
+        C = torch.empty(m, p, dtype=torch.float64, device="cuda")
+        raised = False
+        try:
+            mm.gemm_sharded(m, n, p, torch.float64, A, B, C, layout=mm.MM_ROW_BLOCK)
+            mm.sync_check()
+        except mm.MMError as e:
+            raised = "differ across" in str(e)
+        checks.append({"what": f"collective argument check (mismatch expected: {G > 1})",
+                       "ok": allreduce_ok(raised == (G > 1))})
+    finally:
+        os.environ.pop("MM_CHECK_COLLECTIVE", None)
+
+
 def grids_of(G):
     return [(pr, G // pr) for pr in range(1, G + 1) if G % pr == 0]
 
@@ -247,6 +267,7 @@ def main():
     try:
         row_block_small(G, r, checks)
         summa_small(G, r, checks)
+        collective_check(G, r, checks)
         if args.full:
             c4_full(G, r, checks)
             c5_full(G, r, checks)
