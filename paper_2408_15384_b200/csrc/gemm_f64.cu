@@ -484,6 +484,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
 
 F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
   F64Plan pl;
+  pl.w12 = 0;
   auto tiles = [&](int b) { return ((M + b - 1) / b) * ((N + b - 1) / b); };
   // 128x128 from ~0.6 of a wave of them (16-warp kernels, tools/ab_gpu.py: 96 tiles +2.5 %,
   // 81 even, 64 -5 % vs 64x64); else 32x32 when those fit one wave (every CTA one whole tile,
@@ -498,10 +499,21 @@ F64Plan f64_plan(int64_t M, int64_t N, int64_t K, int num_sms) {
     auto fill = [&](int64_t T) { const int64_t r = T % num_sms; return r == 0 ? 1.0 : (double)r / num_sms; };
     if (t96 <= 4 * (int64_t)num_sms && fill(t96) >= 0.9 && fill(t128) <= 0.75) pl.bm = 96;
   }
-  if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 96 (x128) | 128
+  // Round 2: the big-tile kernel is 96x128 with 12 consumer warps of 32x32 (3 per SM sub-partition +
+  // the producer: 128 registers instead of the 96 that 17 warps leave, no spill): vs 16 warps on
+  // 128x128 / 96x128 tiles, C2 +2.5 %, 4096^3 +0.5 %, 8192^3 +0.2 to +1.3 %, 16384^3 +0.9 %, C5 +0.8 %
+  // (profiles/ab_f64_w12_r2t.txt); 128x96 ties at 8192^3+ but loses 12 % on C2, 96x192 with 32x48
+  // warp tiles 2-10 % slower (profiles/ab_f64_w12_shapes_r2u.txt).
+  if (pl.bm == 128 || pl.bm == 96) {
+    pl.bm = 96;
+    pl.w12 = 1;
+  }
+  if (const char* e = knob("MM_F64_TILE")) {  // tuning knob: 32 | 64 | 96 (x128, 16 warps) | 128 | 9612 (default)
     const int v = atoi(e);
+    pl.w12 = 0;
     if (v == 32 || v == 64 || v == 128) pl.bm = pl.bn = v;
     if (v == 96) { pl.bm = 96; pl.bn = 128; }
+    if (v == 9612) { pl.bm = 96; pl.bn = 128; pl.w12 = 1; }  // (A/B) 12 consumer warps of 32x32
   }
   const int tiles_m = (int)((M + pl.bm - 1) / pl.bm);
   const int tiles_n = (int)((N + pl.bn - 1) / pl.bn);
@@ -550,6 +562,7 @@ void f64_box_dims(const F64Plan& pl, uint32_t* a_box, uint32_t* b_box) {
 
 cudaError_t launch_gemm_f64(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                             const CUtensorMap& tmB3, const GemmArgs& a, const F64Plan& pl, cudaStream_t s) {
+  if (pl.bm == 96 && pl.w12) return launch_impl<96, 128, 3, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
   if (pl.bm == 96) return launch_impl<96, 128, 4, 4, 1>(tmA, tmB, tmA3, tmB3, a, pl, s);
   if (pl.bm == 128) {
     // 16 consumer warps of 32x32 (4 per SM sub-partition, ~96 registers): a warp stalled at a k-block

@@ -37,6 +37,7 @@ struct F64Plan {
   int ks;           // k-block groups of consumer warps (small tiles)
   int kb;           // k-blocks per TMA load (small tiles: 3-D slab maps; 1 = 2-D boxes)
   int ck;           // CTAs per tile along K (2: a cluster splits each tile's K; few small tiles)
+  int w12;          // (A/B) 96x128 tiles with 12 consumer warps of 32x32 (128 registers)
   WorkSched sched;  // whole-tile waves + split tail over sched.nc persistent CTAs
   size_t ws_bytes;
   int flag_count;
