@@ -403,7 +403,9 @@ def per_config_table(mm, peaks, k6=None):
             big = m * n > (1 << 26)
             ck = ClockSampler().start()
             w0 = time.time()
+            mm.clock_meter(True)
             t_ours = per_launch_ms(lambda: mm.gemm(A, B, out=C), reps, None if big else flush)
+            eff_mhz = mm.clock_meter(False)
             w1 = time.time()
             t_ref = per_launch_ms(ref, reps, None if big else flush)
             w2 = time.time()
@@ -413,7 +415,7 @@ def per_config_table(mm, peaks, k6=None):
             tf = flops / t_ours / 1e9
             # SMs x flop/clk/SM (K6-measured) x the SM clock sampled while it ran
             opc, opc_src = flop_per_clk(k6, "f64" if dt == "f64" else "i8", OPS_PER_CLK_SM["f64" if dt == "f64" else "i8"])
-            clock_peak = (SMS * opc * clk_ours["sm_mhz"] * 1e6 / 1e12) if clk_ours else None
+            clock_peak = (SMS * opc * eff_mhz * 1e6 / 1e12) if eff_mhz > 0 else None
             cb = compulsory_bytes(dt, m, n, p)
             dram = (TRAFFIC.get(name) or {}).get("dram_bytes_per_launch")
             hbm = {"compulsory_bytes": cb, "algorithmic_gbs": round(cb / (t_ours * 1e-3) / 1e9, 1),
@@ -435,6 +437,7 @@ def per_config_table(mm, peaks, k6=None):
                 "frac_of_library_peak": round(tf / lib, 4) if lib else None,
                 "frac_of_clock_peak": round(tf / clock_peak, 4) if clock_peak else None,
                 "clock_peak_flop_per_clk_sm": opc, "clock_peak_source": opc_src, "hbm": hbm,
+                "kernel_effective_mhz": round(eff_mhz, 1),
                 "sm_mhz": clk_ours["sm_mhz"] if clk_ours else None,
                 "cublas_sm_mhz": clk_ref["sm_mhz"] if clk_ref else None,
                 "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
@@ -544,6 +547,8 @@ def main():
     ap.add_argument("--no-protocol", action="store_true")
     ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--no-k6", action="store_true")
+    ap.add_argument("--idle-s", type=float, default=0.0,
+                    help="idle seconds between warm-up and the timed region (SURVEY 8(d) d5 burst protocol)")
     ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--threads", type=int, default=1, help=argparse.SUPPRESS)
     ap.add_argument("--config", default=None, help=argparse.SUPPRESS)
@@ -591,11 +596,19 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.idle_s > 0:
+        time.sleep(args.idle_s)
     clk = ClockSampler(local).start()
     win = []
+    mm.clock_meter(True)  # in-kernel effective SM clock (clock64 / globaltimer per CTA), results unchanged
     ms = device_time_steps(step, args.steps, 0, dist, window=win)
+    kernel_mhz = mm.clock_meter(False)
     clk.stop()
     clocks = clk.summary(*win)
+    if clocks is not None:
+        clocks["kernel_effective_mhz_last_step"] = round(kernel_mhz, 1)
+        clocks["kernel_effective_note"] = ("SM cycles / ns over every CTA of the last timed product (mm_clock_meter); "
+                                           "nvidia-smi's sm clock is the requested clock, not the throttled one")
     mm.sync_check()
     launches = mm.launches() - launches0 - args.warmup * (1 if rows > 0 else 0)
     value = flops_total / (ms * 1e-3) / 1e12
@@ -606,11 +619,14 @@ def main():
         n_sus = max(args.steps, int(2000.0 / max(ms, 1e-3)) + 1)
         ck = ClockSampler(local).start()
         w2 = []
+        mm.clock_meter(True)
         ms_sus = device_time_steps(step, n_sus, 0, dist, window=w2)
+        sus_mhz = mm.clock_meter(False)
         ck.stop()
         mm.sync_check()
         sustained = {"steps": n_sus, "seconds": round(ms_sus * n_sus / 1e3, 2), "ms_per_step": round(ms_sus, 4),
                      "value": round(flops_total / (ms_sus * 1e-3) / 1e12, 2), "unit": UNIT, "clocks": ck.summary(*w2),
+                     "kernel_effective_mhz_last_step": round(sus_mhz, 1),
                      "frac_of_sustained_peak": round(flops_total / world / (ms_sus * 1e-3) / 1e12 /
                                                      peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]), 4)}
 
@@ -783,11 +799,17 @@ def main():
                                        "vs_spec_2250": round(value / world / 2250.0, 4),
                                        "vs_clock_normalized": (round(value / world / (
                                            torch.cuda.get_device_properties(0).multi_processor_count *
+                                           flop_per_clk(k6, "bf16", OPS_PER_CLK_SM["bf16"])[0] * kernel_mhz
+                                           * 1e6 / 1e12), 4) if kernel_mhz > 0 else None),
+                                       "vs_clock_normalized_nvidia_smi": (round(value / world / (
+                                           torch.cuda.get_device_properties(0).multi_processor_count *
                                            flop_per_clk(k6, "bf16", OPS_PER_CLK_SM["bf16"])[0] * clocks["sm_mhz"]
                                            * 1e6 / 1e12), 4) if clocks else None),
                                        "clock_normalized_note": "SMs x flop/clk/SM (" +
                                            flop_per_clk(k6, "bf16", OPS_PER_CLK_SM["bf16"])[1] +
-                                           ") x median nvidia-smi SM clock of samples inside the timed region"},
+                                           ") x the in-kernel effective SM clock of the last timed product "
+                                           "(mm_clock_meter); _nvidia_smi: x the median nvidia-smi clock in the "
+                                           "timed region (the requested clock)"},
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

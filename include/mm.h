@@ -242,6 +242,13 @@ mm_status mm_shard_plan(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layo
  * arguments. */
 size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layout layout, int G);
 
+/* Clock meter (measurement): enable = 1 makes every product kernel of this context record, per
+ * CTA, its SM cycle count (clock64) and elapsed nanoseconds (globaltimer) between entry and exit
+ * (four stores per CTA; results unchanged).  enable = 0 synchronises the device, stops recording and
+ * returns in *mhz the effective SM clock of the most recent launch: Σ cycles / Σ ns over its CTAs
+ * (0 if nothing was recorded).  MM_ERR_WORKSPACE if the 128-KiB record buffer cannot be allocated. */
+mm_status mm_clock_meter(mm_ctx* ctx, int enable, double* mhz);
+
 /* Number of kernels this context has launched so far (product, padding and
  * fix-up kernels; NCCL's own kernels are not counted). */
 uint64_t mm_launches(const mm_ctx* ctx);

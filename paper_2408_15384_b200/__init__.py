@@ -22,7 +22,7 @@ from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_GATHER_C_FUS
                    MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
 
 __all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "shard_plan", "workspace_size",
-           "ipc_export", "ipc_open", "MMError", "Context",
+           "ipc_export", "ipc_open", "clock_meter", "MMError", "Context",
            "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
            "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D"]
 
@@ -234,6 +234,15 @@ def gemm_ptr(m: int, n: int, p: int, dtype: torch.dtype, A: int, B: int, C: int,
     ctx = context(device)
     sh = stream.cuda_stream if stream is not None else _raw_stream(device)
     ctx.check(_lib.load().mm_gemm(ctx.handle, m, n, p, IN_DTYPE[dtype], A, B, C, sh))
+
+
+def clock_meter(enable: bool, device: int | None = None) -> float:
+    """mm_clock_meter: start recording (returns 0.0), or stop and return the effective SM clock
+    (MHz) of the most recent product kernel of this thread's context on `device`."""
+    ctx = context(device)
+    mhz = ctypes.c_double()
+    ctx.check(_lib.load().mm_clock_meter(ctx.handle, 1 if enable else 0, ctypes.byref(mhz)))
+    return float(mhz.value)
 
 
 def _nccl_comm_ptr(group) -> int:

@@ -18,7 +18,7 @@ MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE = 1, 2, 4, 8
 EXPORTS = (
     "mm_create", "mm_destroy", "mm_gemm", "mm_gemm_host", "mm_sync_check", "mm_status_string",
     "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_launches", "mm_version",
-    "mm_shard_plan", "mm_workspace_size", "mm_ipc_export", "mm_ipc_open",
+    "mm_shard_plan", "mm_workspace_size", "mm_ipc_export", "mm_ipc_open", "mm_clock_meter",
 )
 
 # mm_plan_op / mm_plan_buf / mm_plan_comm (include/mm.h)
@@ -90,6 +90,8 @@ def load():
     lib.mm_ipc_export.restype = _int
     lib.mm_ipc_open.argtypes = [_vp, ctypes.POINTER(IpcHandle), ctypes.POINTER(_vp)]
     lib.mm_ipc_open.restype = _int
+    lib.mm_clock_meter.argtypes = [_vp, _int, ctypes.POINTER(ctypes.c_double)]
+    lib.mm_clock_meter.restype = _int
     lib.mm_version.argtypes = []
     lib.mm_version.restype = ctypes.c_char_p
     _lib = lib

