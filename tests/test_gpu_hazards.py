@@ -62,10 +62,11 @@ def _exact_ref(tA, tB):
 # (dtype, m, n, p, what it exercises)
 SHARED_CASES = [
     ("bf16", 8192, 8192, 8192, "wave barrier (operands > 96 MB), 512-wide pair tiles"),
-    ("bf16", 2560, 2560, 2560, "reduce-add split tail (mode 3 tickets)"),
+    ("bf16", 2560, 2560, 2560, "N-half split tail (mode 4)"),
+    ("bf16", 4096, 4096, 4096, "reduce-add split tail (mode 3 tickets: the first ticket zeroes C)"),
     ("i8", 4096, 4096, 4096, "configs[2] shape, 256-wide pair tiles"),
     ("f64", 2000, 1500, 1750, "configs[1] shape, FP64 split tail (tickets + publish counts)"),
-    ("f64", 4096, 4096, 4096, "FP64 128x128 tiles, split tail"),
+    ("f64", 4096, 4096, 4096, "FP64 96x128 tiles (12 warps), split tail"),
 ]
 
 
@@ -170,5 +171,3 @@ def test_clock_meter(mm):
         mm.sync_check()
         assert 300.0 < mhz < 2300.0, (dt, mhz)
         assert torch.equal(C.to(torch.float64), ref)
-    C = mm.gemm(tA, tB)  # meter off again: nothing recorded, nothing changed
-    assert mm.clock_meter(False) == 0.0 or True
