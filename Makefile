@@ -61,3 +61,9 @@ K6_LIB := probes/libk6.so
 all: $(K6_LIB)
 $(K6_LIB): probes/k6_peak.cu paper_2408_15384_b200/csrc/ptx.cuh
 	$(NVCC) -std=c++17 -O3 $(GENCODE) -Ipaper_2408_15384_b200/csrc -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -o $@ $<
+
+# test-only NCCL stand-in for several processes on one GPU (tests/test_gpu_shim_multirank.py)
+FAKE_NCCL := tests/libfakenccl.so
+all: $(FAKE_NCCL)
+$(FAKE_NCCL): tests/csrc/fake_nccl.cu
+	$(NVCC) -std=c++17 -O2 $(GENCODE) -Xcompiler -fPIC $(if $(NCCL_INC),-I$(NCCL_INC)) -shared -o $@ $< -L$(CUDA_HOME)/lib64/stubs -lcuda -lrt

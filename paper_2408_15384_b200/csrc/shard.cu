@@ -59,11 +59,11 @@ std::once_flag g_nccl_once;
 
 const NcclApi& nccl() {
   std::call_once(g_nccl_once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOLOAD | RTLD_LAZY);
-    if (!h) {
-      const char* p = getenv("MM_NCCL_LIB");
-      if (p) h = dlopen(p, RTLD_LAZY | RTLD_GLOBAL);
-    }
+    // MM_NCCL_LIB (explicit override, e.g. the test suite's one-GPU shim) first, else the
+    // libnccl.so.2 torch already loaded
+    void* h = nullptr;
+    if (const char* p = getenv("MM_NCCL_LIB")) h = dlopen(p, RTLD_LAZY | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOLOAD | RTLD_LAZY);
     if (!h) return;
 #define LOAD(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name))
     LOAD(Broadcast, "ncclBroadcast");
