@@ -143,7 +143,11 @@ ncclResult_t do_reduce(const void* sbuf, void* rbuf, size_t count, ncclDataType_
   if (root < 0 || c->rank == root) {
     std::vector<char> acc(bytes), x(bytes);
     for (int q = 0; q < (int)c->members.size() && ok; ++q) {  // member order: fixed
-      ok = fetch(g_sh->slots[c->id][q], q == 0 ? acc.data() : x.data(), bytes, true);
+      char* dst = q == 0 ? acc.data() : x.data();
+      if (q == c->rank)  // (an allocation of this process cannot be IPC-opened here)
+        ok = cudaMemcpy(dst, sbuf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess;
+      else
+        ok = fetch(g_sh->slots[c->id][q], dst, bytes, true);
       if (ok && q > 0) combine_any(acc, x, count, dt, op);
     }
     comm_barrier(c);  // every rank has read every send buffer before any is overwritten
