@@ -39,8 +39,8 @@ struct mm_ctx {
   // sharded plans: ROW / COL / DEPTH sub-communicators (ncclComm_t, index = mm_plan_comm), cached
   // per (parent communicator, split colour, key)
   void* sub_comm[4] = {nullptr, nullptr, nullptr, nullptr};
-  int split_color[4] = {-1, -1, -1, -1}, split_key[4] = {-1, -1, -1, -1};
   void* split_parent = nullptr;
+  int64_t split_sig[4] = {-1, -1, -1, -1};  // (layout, grid_rows, grid_cols, G): the same on every rank
   std::vector<cudaEvent_t> plan_events;  // the plan's event ids
   void* sk_ws = nullptr;  // stream-K partial tiles (both kernels)
   size_t sk_ws_bytes = 0;

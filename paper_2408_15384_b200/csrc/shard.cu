@@ -148,23 +148,25 @@ struct PlanBufs {
 };
 
 // Sub-communicators of the plan (ROW / COL / DEPTH), split from WORLD with the plan's colours and
-// keys and cached in the context per (parent, colours, keys).  Every rank takes the same decisions
-// (they depend on the collective's arguments only), so the collective splits stay matched.
-mm_status plan_comms(mm_ctx* ctx, ncclComm_t world, const mm_plan_info& info, ncclComm_t comms[4]) {
+// keys and cached in the context.  ncclCommSplit is collective, so whether to (re-)split must be
+// decided identically on every rank: the cache key is (parent, layout, grid, G) — the collective's
+// arguments — never a rank's own colour or key (two grids can give one rank the same colours and
+// another different ones; keying on colours made only some ranks re-split and deadlocked G > 1,
+// found by tests/test_gpu_shim_multirank.py).
+mm_status plan_comms(mm_ctx* ctx, ncclComm_t world, const mm_plan_info& info, const int64_t sig[4],
+                     ncclComm_t comms[4]) {
   const NcclApi& api = nccl();
   comms[MM_COMM_WORLD] = world;
   bool same = ctx->split_parent == world;
-  for (int c = 1; c < 4; ++c)
-    same = same && ctx->split_color[c] == info.color[c] && ctx->split_key[c] == info.key[c];
+  for (int i = 0; i < 4; ++i) same = same && ctx->split_sig[i] == sig[i];
   if (!same) {
     mm_release_comms(ctx);
     for (int c = 1; c < 4; ++c) {
       ncclComm_t sub = nullptr;
       if (info.color[c] >= 0) NCCL_CHECK(ctx, api.CommSplit(world, info.color[c], info.key[c], &sub, nullptr));
       ctx->sub_comm[c] = sub;
-      ctx->split_color[c] = info.color[c];
-      ctx->split_key[c] = info.key[c];
     }
+    for (int i = 0; i < 4; ++i) ctx->split_sig[i] = sig[i];
     ctx->split_parent = world;
   }
   for (int c = 1; c < 4; ++c) comms[c] = static_cast<ncclComm_t>(ctx->sub_comm[c]);
@@ -174,7 +176,7 @@ mm_status plan_comms(mm_ctx* ctx, ncclComm_t world, const mm_plan_info& info, nc
 // Run rank r's plan: products on the caller's stream (0), communication and staging copies on the
 // context's communication stream (1), ordered by the plan's events.
 mm_status execute_plan(mm_ctx* ctx, const std::vector<mm_plan_step>& steps, const mm_plan_info& info, PlanBufs& B,
-                       mm_dtype dtype, ncclComm_t world, int r, cudaStream_t s0) {
+                       mm_dtype dtype, ncclComm_t world, int r, const int64_t split_sig[4], cudaStream_t s0) {
   const NcclApi& api = nccl();
   // buffers every step needs must exist (usage errors before anything is enqueued)
   for (const mm_plan_step& st : steps) {
@@ -190,7 +192,7 @@ mm_status execute_plan(mm_ctx* ctx, const std::vector<mm_plan_step>& steps, cons
       B.p[MM_BUF_S0 + i] = static_cast<uint8_t*>(ctx->sbuf[i]);
     }
   ncclComm_t comms[4];
-  if ((ss = plan_comms(ctx, world, info, comms)) != MM_OK) return ss;
+  if ((ss = plan_comms(ctx, world, info, split_sig, comms)) != MM_OK) return ss;
   if (!ctx->s_in && cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking) != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "stream creation failed");
   cudaStream_t strm[2] = {s0, ctx->s_in};
@@ -333,8 +335,8 @@ void mm_release_comms(mm_ctx* ctx) {
   for (int c = 1; c < 4; ++c) {
     if (ctx->sub_comm[c] && api.CommDestroy) api.CommDestroy(static_cast<ncclComm_t>(ctx->sub_comm[c]));
     ctx->sub_comm[c] = nullptr;
-    ctx->split_color[c] = ctx->split_key[c] = -1;
   }
+  for (int i = 0; i < 4; ++i) ctx->split_sig[i] = -1;
   ctx->split_parent = nullptr;
 }
 
@@ -431,7 +433,10 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
   B.p[MM_BUF_B] = static_cast<uint8_t*>(B_local);
   B.p[MM_BUF_C] = static_cast<uint8_t*>(C_local);
   B.p[MM_BUF_CFULL] = static_cast<uint8_t*>(C_full);
-  return execute_plan(ctx, steps, info, B, dtype, comm, r, static_cast<cudaStream_t>(stream));
+  // the sub-communicator cache key: identical on every rank (ROW_BLOCK splits nothing)
+  const int64_t sig[4] = {(int64_t)layout, layout == MM_ROW_BLOCK ? 0 : grid_rows, layout == MM_ROW_BLOCK ? 0 : grid_cols,
+                          (int64_t)G};
+  return execute_plan(ctx, steps, info, B, dtype, comm, r, sig, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -26,7 +27,7 @@
 namespace {
 
 constexpr int kMaxRanks = 8;
-constexpr int kMaxComms = 64;
+constexpr int kMaxComms = 256;  // comm id = split sequence * 8 + (colour & 7)
 
 struct Barrier {
   std::atomic<uint32_t> count;
@@ -195,7 +196,12 @@ ncclResult_t flush_p2p(std::vector<Pending>& ops) {
   return ncclSuccess;
 }
 
+bool g_debug = getenv("FAKE_NCCL_DEBUG") != nullptr;
+
 ncclResult_t submit(Pending p, cudaStream_t s) {
+  if (g_debug)
+    fprintf(stderr, "[fake %d] op %d comm %d (rank %d of %zu) bytes %zu peer %d group %d\n", g_world_rank, p.kind,
+            p.comm->id, p.comm->rank, p.comm->members.size(), p.bytes, p.peer, g_group);
   if (cudaStreamSynchronize(s) != cudaSuccess) return ncclUnhandledCudaError;
   if (g_group > 0) {
     g_pending.push_back(p);
@@ -283,6 +289,8 @@ ncclResult_t ncclCommSplit(ncclComm_t comm, int color, int key, ncclComm_t* newc
     if (mem[i].second == g_world_rank) c->rank = (int)i;
   }
   barrier(g_sh->world_bar, g_world_n);
+  if (g_debug) fprintf(stderr, "[fake %d] split seq %d color %d key %d -> id %d rank %d of %zu\n", g_world_rank, seq,
+                       color, key, c->id, c->rank, c->members.size());
   *newcomm = reinterpret_cast<ncclComm_t>(c);
   return ncclSuccess;
 }
