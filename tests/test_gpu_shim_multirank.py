@@ -202,3 +202,89 @@ def test_summa_real_executor(mmod, world, grids):
     if world == 2:
         cases.append((mm.MM_SUMMA_25D, "f64", 297, 450, 283, mm.MM_REPLICATE, 0, (1, 1), None))
     _check(world, cases, _run(world, cases))
+
+
+def _full_worker(rank, world, shm, q):
+    """configs[3] (BF16 16384^3, exact K=3) row-block in the two gather modes and configs[4] (FP64
+    32768^3, exact K=2049) SUMMA 1x2 at G = 2 through the real executor: checksums of the assembled
+    outputs vs SURVEY c7's goldens (offsets beyond 2^32 bytes: C5's blocks are 4 GiB)."""
+    import json
+    os.environ["MM_NCCL_LIB"] = FAKE
+    import paper_2408_15384_b200 as mm
+    from synthgen import gpu as sgg
+    torch.cuda.set_device(0)
+    fake = ctypes.CDLL(FAKE)
+    fake.fake_comm_init.restype = ctypes.c_void_p
+    fake.fake_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+    comm = fake.fake_comm_init(rank, world, shm.encode())
+    lib = mm._lib.load()
+    ctx = mm.context(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_fullsize.json")))
+    res = {}
+    try:
+        N = 16384
+        s, c = mm.shard_range(N, world, rank)
+        A = sgg.exact_bf16(3, sg.ROLE_A, 3, N, N)[s:s + c].contiguous()
+        B = sgg.exact_bf16(3, sg.ROLE_B, 3, N, N)
+        for flags in (mm.MM_BCAST_B | mm.MM_GATHER_C, mm.MM_BCAST_B | mm.MM_GATHER_C_FUSED):
+            Bd = B.clone() if rank == 0 else torch.zeros_like(B)
+            Cl = torch.empty(c, N, dtype=torch.float32, device="cuda")
+            Cf = torch.empty(N, N, dtype=torch.float32, device="cuda") if rank == 0 else None
+            fused = bool(flags & mm.MM_GATHER_C_FUSED)
+            ctx.check(lib.mm_gemm_sharded(ctx.handle, N, N, N, 1, mm.MM_ROW_BLOCK, 0, 0, A.data_ptr(), Bd.data_ptr(),
+                                          None if fused else Cl.data_ptr(), Cf.data_ptr() if Cf is not None else None,
+                                          flags, 0, comm, stream))
+            mm.sync_check()
+            if rank == 0:
+                res[f"C4x3 flags={flags}"] = sg.checksum(Cf.cpu().numpy()) == int(gold["C4x3"]["checksum"], 16)
+            del Bd, Cl, Cf
+        del A, B
+        torch.cuda.empty_cache()
+        N = 32768
+        A5 = sgg.exact_f64(4, sg.ROLE_A, 2049, N, N)
+        B5 = sgg.exact_f64(4, sg.ROLE_B, 2049, N, N)
+        bn = mm.shard_range(N, 2, rank)  # grid 1x2: A column block, B column block
+        Ab = A5[:, bn[0]:bn[0] + bn[1]].contiguous()
+        Bb = B5[:, bn[0]:bn[0] + bn[1]].contiguous()
+        del A5, B5
+        torch.cuda.empty_cache()
+        Cb = torch.empty(N, bn[1], dtype=torch.float64, device="cuda")
+        ctx.check(lib.mm_gemm_sharded(ctx.handle, N, N, N, 0, mm.MM_SUMMA_2D, 1, 2, Ab.data_ptr(), Bb.data_ptr(),
+                                      Cb.data_ptr(), None, 0, 0, comm, stream))
+        mm.sync_check()
+        Ch = Cb.cpu().numpy()
+        cs = 0
+        for i in range(N):
+            cs = (cs + sg.checksum_block(np.ascontiguousarray(Ch[i]), i * N + bn[0], "f64")) % (1 << 64)
+        res["C5x part"] = cs
+        q.put((rank, res))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, {"exc": f"{type(e).__name__}: {e}"}))
+        raise
+
+
+def test_full_size_g2_real_executor(mmod):
+    import json
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    shm = f"/mm_fake_nccl_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_full_worker, args=(r, 2, shm, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    try:
+        res = dict(q.get(timeout=1500) for _ in range(2))
+    finally:
+        for pr in procs:
+            pr.join(timeout=300)
+        try:
+            os.unlink("/dev/shm" + shm)
+        except OSError:
+            pass
+    for r in (0, 1):
+        assert "exc" not in res[r], res[r]
+    for k, v in res[0].items():
+        if k.startswith("C4x3"):
+            assert v, k
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_fullsize.json")))
+    assert (res[0]["C5x part"] + res[1]["C5x part"]) % (1 << 64) == int(gold["C5x"]["checksum"], 16)
