@@ -12,7 +12,6 @@ bit-exact against the oracle on exact-integer inputs.  (tests/test_dist_nccl.py 
 library over real NCCL when a box has >= 2 GPUs.)"""
 import ctypes
 import os
-import socket
 import uuid
 
 import numpy as np
