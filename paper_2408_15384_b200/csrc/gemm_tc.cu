@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // B: MN-major SW128, 128-B (BOXN-column) blocks BOX_BYTES apart (LBO), 8-row k groups 1024 B (SBO).
             const uint64_t bdesc =
                 umma_desc_sw128(sb + rr * Cfg::REGION_BYTES + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-            if (lane == 0) tc_mma<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (!first_kb || kk != 0) ? 1u : 0u);
+            tc_mma_warp<CG, I8>(d_tmem + rr * kBN, adesc, bdesc, Cfg::IDESC, (!first_kb || kk != 0) ? 1u : 0u);
           }
         }
       };
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // B: MN-major, one 64-column block per CTA: bf16 rows of 128 B (SW128), int8 rows of 64 B (SW64)
           const uint64_t bdesc = I8 ? umma_desc_sw64(sb + kk * Cfg::UK * 64, Cfg::HB_BYTES, 512)
                                     : umma_desc_sw128(sb + kk * Cfg::UK * 128, Cfg::BOX_BYTES, 1024);
-          if (lane == 0) tc_mma<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC_H, (!first_kb || kk != 0) ? 1u : 0u);
+          tc_mma_warp<CG, I8>(d_tmem, adesc, bdesc, Cfg::IDESC_H, (!first_kb || kk != 0) ? 1u : 0u);
         }
       };
       auto wait_tempty = [&](int a, uint32_t parity) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase = p0;
           for (int i = 0; i < pre; ++i) {
             issue(d_tmem, stage, i == 0, 1, 2);
-            if (lane == 0) tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+            tc_commit_warp<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
             __syncwarp();
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
           }
@@ -418,13 +418,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           else issue(d_tmem, stage, kb == kb0, 0, NT);
           // frees this smem stage when the MMAs retire: in both CTAs of the pair, and with MC = 2 also
           // in the other pair, whose producers multicast into this pair's slots
-          if (lane == 0) tc_commit<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
+          tc_commit_warp<CG>(empty_bar(stage), MC == 2 ? (uint16_t)0xF : (uint16_t)0x3);
           __syncwarp();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
         if (!ok) break;
         if (tl && lane == 0 && j < 8) tl[4 * j + 1] = globaltimer_ns();
-        if (lane == 0) tc_commit<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs)
+        tc_commit_warp<CG>(tfull_bar(acc), (uint16_t)(0x3u << leader));  // accumulator ready (both CTAs)
         __syncwarp();
       }
     }

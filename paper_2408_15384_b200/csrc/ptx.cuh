@@ -358,6 +358,42 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
         : "memory");
 }
 
+// The same MMA called by the WHOLE (converged) warp: one lane, picked by elect.sync inside the asm,
+// issues it.  Keeping the call site convergent lets ptxas hold the descriptors in uniform
+// registers; a call under `if (lane == 0)` made every MMA a waterfall (ELECT / R2UR.BROADCAST /
+// BRA.U.ANY, ~14 instructions) that bounded the issue rate of short (N = 128) MMAs.
+#define MMB_TC_MMA_WARP(CGS, KIND)                                                                  \
+  asm volatile(                                                                                     \
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"                                                   \
+      "elect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                    \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::" KIND " [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem), \
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)                                                \
+      : "memory")
+template <int CG, bool I8>
+__device__ __forceinline__ void tc_mma_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  if constexpr (CG == 1 && !I8) MMB_TC_MMA_WARP("1", "f16");
+  else if constexpr (CG == 2 && !I8) MMB_TC_MMA_WARP("2", "f16");
+  else if constexpr (CG == 1 && I8) MMB_TC_MMA_WARP("1", "i8");
+  else MMB_TC_MMA_WARP("2", "i8");
+}
+#undef MMB_TC_MMA_WARP
+// tc_commit called by the whole warp, one elected lane commits (see tc_mma_warp)
+template <int CG>
+__device__ __forceinline__ void tc_commit_warp(uint32_t bar, uint16_t cta_mask = 0x3) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+        "h"(cta_mask)
+        : "memory");
+}
+
 // Arrive on `bar` once all prior tcgen05 ops of this thread complete.
 // CG==2: multicast to the same barrier offset in every CTA of `cta_mask`.
 template <int CG>
