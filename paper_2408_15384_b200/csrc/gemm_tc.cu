@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           kb = kb0 + pre;
         } else {
           if (!wait_tempty(acc, (use & 1u) ^ 1u)) { ok = false; break; }
+          // (MM_EXP bit 0: the previous tile's read-out finishes before this tile's MMAs start)
+          if ((args.exp & 1) && j > 0 && !wait_tempty(acc ^ 1, ((uint32_t)((j - 1) / 2) & 1u))) { ok = false; break; }
         }
         const bool half_item = NT == 1 && CG == 2 && MC == 1 && sched.half_of(cl, j) >= 0;
         for (; kb < kb1; ++kb) {

@@ -29,6 +29,7 @@ struct GemmArgs {
   unsigned long long* trace;  // optional per-CTA wait-time counters (16 per CTA), MM_TRACE=1
   int debug;        // diagnostics only (MM_DEBUG): bit 0 = tcgen05 producer skips the operand loads
   int ka;           // tcgen05 kernel: 128-B K atoms per stage (1, or 2 for 256-wide pair tiles)
+  int exp;          // schedule experiments that keep results exact (knob MM_EXP, A/B only; 0 = off)
   unsigned long long* clk;  // clock meter (mm_clock_meter): per CTA {clock64, globaltimer} at entry and exit, or null
 };
 

@@ -302,6 +302,8 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     a.trace = static_cast<unsigned long long*>(ctx->trace_buf);
   }
   if (const char* env = knob("MM_L2_HINT")) a.l2_hint = atoi(env);  // tuning knob
+  a.exp = 0;
+  if (const char* env = knob("MM_EXP")) a.exp = atoi(env);  // (A/B knob: schedule experiments)
   // stream-K workspace (partial tiles) + self-resetting per-tile counters, shared by both kernels
   auto ensure_sk = [&](size_t ws_bytes, size_t flag_count) -> mm_status {
     if (ctx->sk_flag_count < flag_count) {
@@ -394,7 +396,20 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     // With few waves of 512-wide tiles (quantisation, an exposed read-out per tile) 256-wide tiles
     // with TMEM double-buffering and two K atoms per stage win: int8 4096^3 +3 %, bf16 4096^3 +2 %;
     // from ~7 waves on (8192^3) 512-wide tiles stay ahead (tools/ab_gpu.py).
-    if (nt == 2 && !a.wave_sync && mc == 1 && tiles_nt2 < 3 * (num_sms / 2)) nt = 1;
+    // Round 2 (after the warp-elected MMA issue, 256- and 512-wide tiles run at the same rate per
+    // FLOP up to ~8 waves): pick the width with fewer rounds of work per cluster; 256-wide rounds
+    // count half, a partial last round of them that fits the N-half split (tail <= nc/2) 0.4;
+    // ties go to 512-wide tiles (fewer DRAM re-reads).  Measured: int8 4096x4096x8192 / 8192x4096x4096
+    // +14 / +16 %, bf16 4096x4096x8192 +4 % (3.46 waves of 512-wide tiles: 4 rounds vs 3.5);
+    // int8 6144^3 equal (4 vs 4) (profiles/ab_nt_rounds_r2zi.txt).
+    if (nt == 2 && !a.wave_sync && mc == 1) {
+      const int64_t nc = std::max(1, num_sms / 2);
+      const int64_t tiles_nt1 = ((m + 255) / 256) * ((p + 255) / 256);
+      const double r2 = (double)((tiles_nt2 + nc - 1) / nc);
+      const int64_t tail1 = tiles_nt1 % nc;
+      const double r1 = 0.5 * (double)(tiles_nt1 / nc) + (tail1 == 0 ? 0.0 : (2 * tail1 <= nc ? 0.4 : 0.5));
+      if (r1 < r2) nt = 1;
+    }
     if (const char* env = knob("MM_NT")) nt = (cg == 2 && atoi(env) == 2) ? 2 : 1;  // tuning knob
     // 256-wide pair tiles: two 128-B K atoms per stage — 8 MMAs per barrier wait and commit instead
     // of 4 (the single issuing thread, not the tensor pipe, bounded 4-MMA stages at ~75 % busy)

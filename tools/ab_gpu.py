@@ -94,8 +94,10 @@ def main():
             assert lib.mm_sync_check(h, s) == 0
         fl = 2.0 * m * n * p
         ma, mb = statistics.median(res["A"]), statistics.median(res["B"])
+        # CUDA event times on this pool come in ~2-us steps: the mean over reps resolves finer
+        xa, xb = statistics.fmean(res["A"]), statistics.fmean(res["B"])
         print(f"{case:>22s}: A {ma*1e3:9.1f} us ({fl/ma/1e9:7.1f} TF)  B {mb*1e3:9.1f} us ({fl/mb/1e9:7.1f} TF)  "
-              f"B/A speed {ma/mb:5.3f}", flush=True)
+              f"B/A speed {ma/mb:5.3f}  | means A {xa*1e3:9.2f} B {xb*1e3:9.2f} us, B/A speed {xa/xb:5.3f}", flush=True)
         del A, B, C
         torch.cuda.empty_cache()
 
