@@ -110,6 +110,11 @@ const char* mm_last_error(const mm_ctx* ctx);
  *          transfer overlaps the math tile by tile; C_local is not written
  *          (may be NULL).  Ends with a communicator-wide barrier so C_full is
  *          complete on `root` when the call's stream work finishes.
+ *          MM_C_WINDOW (with MM_GATHER_C_FUSED): the peer mapping is NCCL's
+ *          instead — every rank passes, as C_full, its own buffer from
+ *          mm_window_alloc at the same offset (symmetric memory), and the root's
+ *          address comes from the window (ncclGetPeerPointer, NCCL's LSA/NVLink
+ *          mapping) with no handle exchange.
  * MM_SUMMA_2D: ranks form a grid_rows × grid_cols grid (G = grid_rows*grid_cols),
  *   rank r ↔ (r / grid_cols, r % grid_cols).  Rank (i,j) owns block (i,j)
  *   of A (row block i of m, column block j of n), of B (row block i of n,
@@ -133,7 +138,7 @@ const char* mm_last_error(const mm_ctx* ctx);
  * time from the libnccl.so.2 already loaded in the process.
  */
 typedef enum { MM_ROW_BLOCK = 0, MM_SUMMA_2D = 1, MM_SUMMA_25D = 2 } mm_layout;
-enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u, MM_GATHER_C_FUSED = 4u, MM_REPLICATE = 8u };
+enum { MM_BCAST_B = 1u, MM_GATHER_C = 2u, MM_GATHER_C_FUSED = 4u, MM_REPLICATE = 8u, MM_C_WINDOW = 16u };
 
 mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                           mm_layout layout, int grid_rows, int grid_cols,
@@ -150,6 +155,16 @@ mm_status mm_gemm_sharded(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype
 typedef struct { unsigned char bytes[72]; } mm_ipc_handle;
 mm_status mm_ipc_export(mm_ctx* ctx, const void* dev_ptr, mm_ipc_handle* out);
 mm_status mm_ipc_open(mm_ctx* ctx, const mm_ipc_handle* handle, void** dev_ptr);
+
+/* NCCL symmetric memory for MM_GATHER_C_FUSED | MM_C_WINDOW (PAPER.md:135/146 —
+ * communication between the processes of a node).  Collective over nccl_comm (every rank, same
+ * `bytes`): allocates `bytes` with ncclMemAlloc (cuMem VMM memory NCCL can map into its peers)
+ * and registers it as a window (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC); *ptr receives
+ * this rank's buffer.  The context records (buffer, window, communicator); the caller frees it
+ * with mm_window_free (collective, same order on every rank) before mm_destroy.
+ * MM_ERR_UNSUPPORTED if the loaded NCCL has no window API; MM_ERR_RUNTIME on NCCL failure. */
+mm_status mm_window_alloc(mm_ctx* ctx, void* nccl_comm, size_t bytes, void** ptr);
+mm_status mm_window_free(mm_ctx* ctx, void* ptr);
 
 /* Contiguous block partition of `total` items over G parts:
  * part r gets [start, start+count); the first parts get ⌈total/G⌉, the

@@ -18,13 +18,14 @@ import threading
 import torch
 
 from . import _lib
-from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE, MM_ROW_BLOCK,
-                   MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
+from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_C_WINDOW, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE,
+                   MM_ROW_BLOCK, MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
 
 __all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "shard_plan", "workspace_size",
-           "ipc_export", "ipc_open", "clock_meter", "MMError", "Context",
+           "ipc_export", "ipc_open", "window_alloc", "window_free", "clock_meter", "MMError", "Context",
            "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
-           "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D"]
+           "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D",
+           "MM_C_WINDOW"]
 
 IN_DTYPE = {torch.float64: MM_F64, torch.bfloat16: MM_BF16_F32, torch.int8: MM_S8_S32}
 OUT_DTYPE = {MM_F64: torch.float64, MM_BF16_F32: torch.float32, MM_S8_S32: torch.int32}
@@ -226,6 +227,38 @@ def ipc_open(handle: bytes, device: int = 0) -> int:
     ptr = ctypes.c_void_p()
     ctx.check(_lib.load().mm_ipc_open(ctx.handle, ctypes.byref(h), ctypes.byref(ptr)))
     return int(ptr.value)
+
+
+class _DevBuf:
+    """A raw device buffer seen through __cuda_array_interface__ (torch.as_tensor wraps it, no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+_TYPESTR = {torch.float64: "<f8", torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<i2", torch.int8: "|i1"}
+
+
+def window_alloc(shape, dtype: torch.dtype, group=None, device: int | None = None) -> torch.Tensor:
+    """Collective (mm_window_alloc): NCCL symmetric memory for MM_GATHER_C_FUSED | MM_C_WINDOW,
+    returned as a tensor viewing this rank's buffer.  Free it with window_free (collective)."""
+    dev = torch.cuda.current_device() if device is None else device
+    ctx = context(dev)
+    numel = 1
+    for d in shape:
+        numel *= int(d)
+    nbytes = numel * torch.empty(0, dtype=dtype).element_size()
+    ptr = ctypes.c_void_p()
+    ctx.check(_lib.load().mm_window_alloc(ctx.handle, _nccl_comm_ptr(group), nbytes, ctypes.byref(ptr)))
+    t = torch.as_tensor(_DevBuf(int(ptr.value), shape, _TYPESTR[dtype]), device=torch.device("cuda", dev))
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
+def window_free(t: torch.Tensor):
+    """Collective (mm_window_free): deregister and free a window_alloc buffer."""
+    ctx = context(t.device.index)
+    ctx.check(_lib.load().mm_window_free(ctx.handle, t.data_ptr()))
 
 
 def gemm_ptr(m: int, n: int, p: int, dtype: torch.dtype, A: int, B: int, C: int, device: int = 0,

@@ -12,13 +12,14 @@ LIB_PATH = os.environ.get("MM_B200_LIB") or os.path.join(_HERE, "libmm_b200.so")
 MM_F64, MM_BF16_F32, MM_S8_S32 = 0, 1, 2
 MM_OK, MM_ERR_RUNTIME, MM_ERR_USAGE, MM_ERR_UNSUPPORTED, MM_ERR_WORKSPACE = 0, 1, 2, 3, 4
 MM_ROW_BLOCK, MM_SUMMA_2D, MM_SUMMA_25D = 0, 1, 2
-MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE = 1, 2, 4, 8
+MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE, MM_C_WINDOW = 1, 2, 4, 8, 16
 
 # every symbol include/mm.h declares
 EXPORTS = (
     "mm_create", "mm_destroy", "mm_gemm", "mm_gemm_host", "mm_sync_check", "mm_status_string",
     "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_launches", "mm_version",
     "mm_shard_plan", "mm_workspace_size", "mm_ipc_export", "mm_ipc_open", "mm_clock_meter",
+    "mm_window_alloc", "mm_window_free",
 )
 
 # mm_plan_op / mm_plan_buf / mm_plan_comm (include/mm.h)
@@ -90,6 +91,10 @@ def load():
     lib.mm_ipc_export.restype = _int
     lib.mm_ipc_open.argtypes = [_vp, ctypes.POINTER(IpcHandle), ctypes.POINTER(_vp)]
     lib.mm_ipc_open.restype = _int
+    lib.mm_window_alloc.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.POINTER(_vp)]
+    lib.mm_window_alloc.restype = _int
+    lib.mm_window_free.argtypes = [_vp, _vp]
+    lib.mm_window_free.restype = _int
     lib.mm_clock_meter.argtypes = [_vp, _int, ctypes.POINTER(ctypes.c_double)]
     lib.mm_clock_meter.restype = _int
     lib.mm_version.argtypes = []

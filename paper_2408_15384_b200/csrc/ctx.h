@@ -53,6 +53,13 @@ struct mm_ctx {
     size_t bytes;
   };
   std::vector<IpcMap> ipc_open;  // allocations of other processes mapped by mm_ipc_open
+  struct Window {  // mm_window_alloc: NCCL symmetric memory of this rank
+    void* base;
+    size_t bytes;
+    void* win;   // ncclWindow_t
+    void* comm;  // ncclComm_t it is registered with
+  };
+  std::vector<Window> windows;
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   unsigned long long* clk_buf = nullptr;  // clock meter: 4096 CTAs x {c0, t0, c1, t1} of the last launch

@@ -276,8 +276,9 @@ __attribute__((visibility("default"))) mm_status mm_shard_plan(int64_t m, int64_
   Builder b;
   if (layout == MM_ROW_BLOCK) {
     if (root < 0 || root >= G) return MM_ERR_USAGE;
-    if (flags & ~(unsigned)(MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED)) return MM_ERR_USAGE;
+    if (flags & ~(unsigned)(MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED | MM_C_WINDOW)) return MM_ERR_USAGE;
     if ((flags & MM_GATHER_C) && (flags & MM_GATHER_C_FUSED)) return MM_ERR_USAGE;
+    if ((flags & MM_C_WINDOW) && !(flags & MM_GATHER_C_FUSED)) return MM_ERR_USAGE;  // (executor detail only)
     row_block(b, info, m, n, p, dtype, flags, root, G, r, panel);
   } else if (layout == MM_SUMMA_2D || layout == MM_SUMMA_25D) {
     if (dtype != MM_F64) return MM_ERR_UNSUPPORTED;  // panels accumulate with beta = 1 (FP64 kernel)

@@ -34,6 +34,7 @@
 #include "ctx.h"
 #include "kernels.h"
 #include "knobs.h"
+#include <nccl_device.h>  // ncclGetPeerPointer (header-only device helper over a registered window)
 
 namespace mmb {
 namespace {
@@ -52,12 +53,17 @@ struct NcclApi {
   ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // symmetric memory (NCCL >= 2.27; optional: MM_C_WINDOW needs them)
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
   bool ok = false;
 };
 NcclApi g_nccl;
 std::once_flag g_nccl_once;
 
-const NcclApi& nccl() {
+const NcclApi& nccl_api() {
   std::call_once(g_nccl_once, [] {
     // MM_NCCL_LIB (explicit override, e.g. the test suite's one-GPU shim) first, else the
     // libnccl.so.2 torch already loaded
@@ -78,6 +84,10 @@ const NcclApi& nccl() {
     LOAD(CommCount, "ncclCommCount");
     LOAD(CommUserRank, "ncclCommUserRank");
     LOAD(GetErrorString, "ncclGetErrorString");
+    LOAD(MemAlloc, "ncclMemAlloc");
+    LOAD(MemFree, "ncclMemFree");
+    LOAD(CommWindowRegister, "ncclCommWindowRegister");
+    LOAD(CommWindowDeregister, "ncclCommWindowDeregister");
 #undef LOAD
     g_nccl.ok = g_nccl.Broadcast && g_nccl.AllReduce && g_nccl.Reduce && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd &&
                 g_nccl.CommSplit && g_nccl.CommCount && g_nccl.CommUserRank && g_nccl.GetErrorString;
@@ -89,7 +99,7 @@ const NcclApi& nccl() {
   do {                                                                                                      \
     ncclResult_t _r = (call);                                                                               \
     if (_r != ncclSuccess)                                                                                  \
-      return set_err(ctx, MM_ERR_RUNTIME, "%s failed: %s", #call, nccl().GetErrorString(_r));               \
+      return set_err(ctx, MM_ERR_RUNTIME, "%s failed: %s", #call, nccl_api().GetErrorString(_r));               \
   } while (0)
 
 // cuMemGetAddressRange from the driver (base + size of the allocation holding a pointer).
@@ -123,7 +133,7 @@ mm_status peer_pointer_of_root(mm_ctx* ctx, void* root_ptr, int root, int r, ncc
     return set_err(ctx, MM_ERR_WORKSPACE, "IPC exchange buffer allocation failed");
   if (r == root && cudaMemcpyAsync(ctx->ipc_xchg, &msg, sizeof msg, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "IPC handle staging failed");
-  NCCL_CHECK(ctx, nccl().Broadcast(ctx->ipc_xchg, ctx->ipc_xchg, sizeof msg, ncclUint8, root, comm, s));
+  NCCL_CHECK(ctx, nccl_api().Broadcast(ctx->ipc_xchg, ctx->ipc_xchg, sizeof msg, ncclUint8, root, comm, s));
   if (cudaMemcpyAsync(&msg, ctx->ipc_xchg, sizeof msg, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
     return set_err(ctx, MM_ERR_RUNTIME, "IPC handle exchange failed");
@@ -138,8 +148,37 @@ mm_status peer_pointer_of_root(mm_ctx* ctx, void* root_ptr, int root, int r, ncc
   return MM_OK;
 }
 
+// The root's address of a symmetric buffer: NCCL maps every rank's window of a node into one flat
+// range of this process (LSA, over NVLink); ncclGetPeerPointer reads the window's device-side
+// descriptor, so it runs on the device.
+__global__ void window_peer_ptr_kernel(ncclWindow_t w, size_t off, int peer, void** out) {
+  *out = ncclGetPeerPointer(w, off, peer);
+}
+
+// MM_C_WINDOW: every rank's C_full lies in a window of this context at the same offset; the root's
+// copy is at ncclGetPeerPointer(window, offset, root).  Local, no communication.
+mm_status window_pointer_of_root(mm_ctx* ctx, void* my_ptr, int root, cudaStream_t s, uint8_t** out) {
+  const mm_ctx::Window* w = nullptr;
+  for (const auto& e : ctx->windows)
+    if (static_cast<uint8_t*>(my_ptr) >= static_cast<uint8_t*>(e.base) &&
+        static_cast<uint8_t*>(my_ptr) < static_cast<uint8_t*>(e.base) + e.bytes)
+      w = &e;
+  if (!w) return set_err(ctx, MM_ERR_USAGE, "MM_C_WINDOW: C_full %p is not in a buffer from mm_window_alloc", my_ptr);
+  const size_t off = static_cast<size_t>(static_cast<uint8_t*>(my_ptr) - static_cast<uint8_t*>(w->base));
+  if (!ctx->ipc_xchg && cudaMalloc(&ctx->ipc_xchg, 256) != cudaSuccess)
+    return set_err(ctx, MM_ERR_WORKSPACE, "window pointer staging allocation failed");
+  window_peer_ptr_kernel<<<1, 1, 0, s>>>(static_cast<ncclWindow_t>(w->win), off, root, static_cast<void**>(ctx->ipc_xchg));
+  void* p = nullptr;
+  if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(&p, ctx->ipc_xchg, sizeof p, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess || !p)
+    return set_err(ctx, MM_ERR_RUNTIME, "MM_C_WINDOW: resolving the root's window address failed");
+  *out = static_cast<uint8_t*>(p);
+  return MM_OK;
+}
+
 // The executor's view of a plan's buffers.
 struct PlanBufs {
+  bool c_window = false;  // MM_C_WINDOW: the fused gather's peer address comes from an NCCL window
   uint8_t* p[10] = {};
   const char* name(int b) const {
     static const char* n[10] = {"-", "A_local", "B_local", "C_local", "C_full", "C_peer", "S0", "S1", "S2", "S3"};
@@ -155,7 +194,7 @@ struct PlanBufs {
 // found by tests/test_gpu_shim_multirank.py).
 mm_status plan_comms(mm_ctx* ctx, ncclComm_t world, const mm_plan_info& info, const int64_t sig[4],
                      ncclComm_t comms[4]) {
-  const NcclApi& api = nccl();
+  const NcclApi& api = nccl_api();
   comms[MM_COMM_WORLD] = world;
   bool same = ctx->split_parent == world;
   for (int i = 0; i < 4; ++i) same = same && ctx->split_sig[i] == sig[i];
@@ -177,7 +216,7 @@ mm_status plan_comms(mm_ctx* ctx, ncclComm_t world, const mm_plan_info& info, co
 // context's communication stream (1), ordered by the plan's events.
 mm_status execute_plan(mm_ctx* ctx, const std::vector<mm_plan_step>& steps, const mm_plan_info& info, PlanBufs& B,
                        mm_dtype dtype, ncclComm_t world, int r, const int64_t split_sig[4], cudaStream_t s0) {
-  const NcclApi& api = nccl();
+  const NcclApi& api = nccl_api();
   // buffers every step needs must exist (usage errors before anything is enqueued)
   for (const mm_plan_step& st : steps) {
     const int need[3] = {st.dst, st.src, st.src2};
@@ -253,7 +292,8 @@ mm_status execute_plan(mm_ctx* ctx, const std::vector<mm_plan_step>& steps, cons
         break;
       case MM_OP_MAP_PEER: {
         uint8_t* peer = nullptr;
-        mm_status g = peer_pointer_of_root(ctx, B.p[MM_BUF_CFULL], st.peer, r, world, sx, &peer);
+        mm_status g = B.c_window ? window_pointer_of_root(ctx, B.p[MM_BUF_CFULL], st.peer, sx, &peer)
+                                 : peer_pointer_of_root(ctx, B.p[MM_BUF_CFULL], st.peer, r, world, sx, &peer);
         if (g != MM_OK) return g;
         B.p[MM_BUF_CPEER] = peer;
         break;
@@ -280,6 +320,43 @@ mm_status execute_plan(mm_ctx* ctx, const std::vector<mm_plan_step>& steps, cons
 using namespace mmb;
 
 extern "C" {
+
+__attribute__((visibility("default"))) mm_status mm_window_alloc(mm_ctx* ctx, void* nccl_comm, size_t bytes, void** ptr) {
+  if (!ctx || !nccl_comm || !ptr || bytes == 0)
+    return ctx ? set_err(ctx, MM_ERR_USAGE, "mm_window_alloc: NULL argument or zero bytes") : MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return set_err(ctx, MM_ERR_RUNTIME, "libnccl.so.2 is not loaded in this process");
+  if (!api.MemAlloc || !api.MemFree || !api.CommWindowRegister || !api.CommWindowDeregister)
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "the loaded NCCL has no symmetric-memory window API");
+  void* p = nullptr;
+  NCCL_CHECK(ctx, api.MemAlloc(&p, bytes));
+  ncclWindow_t w = nullptr;
+  ncclResult_t rr = api.CommWindowRegister(static_cast<ncclComm_t>(nccl_comm), p, bytes, &w, NCCL_WIN_COLL_SYMMETRIC);
+  if (rr != ncclSuccess) {
+    api.MemFree(p);
+    return set_err(ctx, MM_ERR_RUNTIME, "ncclCommWindowRegister failed: %s", api.GetErrorString(rr));
+  }
+  ctx->windows.push_back({p, bytes, static_cast<void*>(w), nccl_comm});
+  *ptr = p;
+  return MM_OK;
+}
+
+__attribute__((visibility("default"))) mm_status mm_window_free(mm_ctx* ctx, void* ptr) {
+  if (!ctx || !ptr) return ctx ? set_err(ctx, MM_ERR_USAGE, "mm_window_free: NULL argument") : MM_ERR_USAGE;
+  DeviceGuard dg(ctx->device);
+  const NcclApi& api = nccl_api();
+  for (size_t i = 0; i < ctx->windows.size(); ++i) {
+    const mm_ctx::Window e = ctx->windows[i];
+    if (e.base != ptr) continue;
+    ctx->windows.erase(ctx->windows.begin() + (ptrdiff_t)i);
+    cudaDeviceSynchronize();  // no product may still store into it
+    NCCL_CHECK(ctx, api.CommWindowDeregister(static_cast<ncclComm_t>(e.comm), static_cast<ncclWindow_t>(e.win)));
+    NCCL_CHECK(ctx, api.MemFree(e.base));
+    return MM_OK;
+  }
+  return set_err(ctx, MM_ERR_USAGE, "mm_window_free: %p was not returned by mm_window_alloc on this context", ptr);
+}
 
 __attribute__((visibility("default"))) mm_status mm_ipc_export(mm_ctx* ctx, const void* dev_ptr, mm_ipc_handle* out) {
   if (!ctx || !dev_ptr || !out) return ctx ? set_err(ctx, MM_ERR_USAGE, "mm_ipc_export: NULL argument") : MM_ERR_USAGE;
@@ -331,7 +408,7 @@ __attribute__((visibility("default"))) mm_status mm_ipc_open(mm_ctx* ctx, const 
 
 void mm_release_comms(mm_ctx* ctx) {
   if (!ctx) return;
-  const NcclApi& api = nccl();
+  const NcclApi& api = nccl_api();
   for (int c = 1; c < 4; ++c) {
     if (ctx->sub_comm[c] && api.CommDestroy) api.CommDestroy(static_cast<ncclComm_t>(ctx->sub_comm[c]));
     ctx->sub_comm[c] = nullptr;
@@ -365,7 +442,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
   if (!nccl_comm) return set_err(ctx, MM_ERR_USAGE, "nccl_comm is NULL");
   mm_status st = refuse_diag_knobs(ctx);
   if (st != MM_OK) return st;
-  const NcclApi& api = nccl();
+  const NcclApi& api = nccl_api();
   if (!api.ok)
     return set_err(ctx, MM_ERR_RUNTIME, "libnccl.so.2 is not loaded in this process (set MM_NCCL_LIB to override)");
   ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
@@ -405,8 +482,12 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
     if (!B_local) return set_err(ctx, MM_ERR_USAGE, "B_local is NULL");
     if ((flags & MM_GATHER_C) && (flags & MM_GATHER_C_FUSED))
       return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C and MM_GATHER_C_FUSED are exclusive");
-    if (flags & ~(unsigned)(MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED))
-      return set_err(ctx, MM_ERR_USAGE, "MM_ROW_BLOCK takes MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED only");
+    if (flags & ~(unsigned)(MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED | MM_C_WINDOW))
+      return set_err(ctx, MM_ERR_USAGE, "MM_ROW_BLOCK takes MM_BCAST_B | MM_GATHER_C | MM_GATHER_C_FUSED | MM_C_WINDOW only");
+    if ((flags & MM_C_WINDOW) && !(flags & MM_GATHER_C_FUSED))
+      return set_err(ctx, MM_ERR_USAGE, "MM_C_WINDOW applies to MM_GATHER_C_FUSED only");
+    if ((flags & MM_C_WINDOW) && !C_full)
+      return set_err(ctx, MM_ERR_USAGE, "MM_C_WINDOW: every rank passes its own window buffer as C_full (NULL on rank %d)", r);
     if ((flags & (MM_GATHER_C | MM_GATHER_C_FUSED)) && r == root && !C_full)
       return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C / MM_GATHER_C_FUSED need C_full on the root rank");
   } else if (layout == MM_SUMMA_2D || layout == MM_SUMMA_25D) {
@@ -433,6 +514,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
   B.p[MM_BUF_B] = static_cast<uint8_t*>(B_local);
   B.p[MM_BUF_C] = static_cast<uint8_t*>(C_local);
   B.p[MM_BUF_CFULL] = static_cast<uint8_t*>(C_full);
+  B.c_window = layout == MM_ROW_BLOCK && (flags & MM_C_WINDOW);
   // the sub-communicator cache key: identical on every rank (ROW_BLOCK splits nothing)
   const int64_t sig[4] = {(int64_t)layout, layout == MM_ROW_BLOCK ? 0 : grid_rows, layout == MM_ROW_BLOCK ? 0 : grid_cols,
                           (int64_t)G};

@@ -7,7 +7,8 @@ prints one JSON line {"ok": bool, "checks": [...]} at the end.  Checks (PAPER.md
 partition, PAPER.md:135 SUMMA / 2.5D; BASELINE.json configs[3] at G = 1/2/4/8, configs[4] over the
 1x2 / 2x2 / 2x4 grids):
   * row-block products of ragged exact-integer shapes with every flag combination
-    (resident, MM_BCAST_B, MM_GATHER_C, both, MM_GATHER_C_FUSED, MM_BCAST_B | MM_GATHER_C_FUSED),
+    (resident, MM_BCAST_B, MM_GATHER_C, both, MM_GATHER_C_FUSED, MM_BCAST_B | MM_GATHER_C_FUSED, the same with
+    MM_C_WINDOW: NCCL symmetric memory instead of a CUDA-IPC mapping),
     every dtype: C_local per rank, C_full on the root and B_local afterwards, bit-exact vs the oracle;
   * SUMMA over every grid G factors into, and 2.5D over every (grid, layers) — FP64, exact;
   * --full: configs[3] (BF16 16384^3) on exact-integer inputs K=3 in the three gather modes: the
@@ -75,7 +76,7 @@ def block_checksum(C: np.ndarray, r0: int, c0: int, p: int, kind: str) -> int:
 
 def row_block_small(G, r, checks):
     flags_list = [0, mm.MM_BCAST_B, mm.MM_GATHER_C, mm.MM_BCAST_B | mm.MM_GATHER_C, mm.MM_GATHER_C_FUSED,
-                  mm.MM_BCAST_B | mm.MM_GATHER_C_FUSED]
+                  mm.MM_BCAST_B | mm.MM_GATHER_C_FUSED, mm.MM_BCAST_B | mm.MM_GATHER_C_FUSED | mm.MM_C_WINDOW]
     for dt in ("bf16", "i8", "f64"):
         m, n, p = 1000 + 13 * G, 768, 1100
         A = exact_host(dt, 61, KEXACT[dt], m, n, 1)
@@ -88,7 +89,13 @@ def row_block_small(G, r, checks):
             Bd = to_dev(B, dt) if (r == root or not flags & mm.MM_BCAST_B) else torch.zeros(n, p, dtype=TORCH_IN[dt],
                                                                                           device="cuda")
             Cl = torch.full((c, p), -9, dtype=TORCH_OUT[dt], device="cuda")
-            Cf = torch.full((m, p), -9, dtype=TORCH_OUT[dt], device="cuda") if r == root else None
+            win = None
+            if flags & mm.MM_C_WINDOW:  # NCCL symmetric memory on every rank, C_full at the same offset
+                win = mm.window_alloc((m + 2, p), TORCH_OUT[dt])
+                win.fill_(-9)
+                Cf = win[1:1 + m]
+            else:
+                Cf = torch.full((m, p), -9, dtype=TORCH_OUT[dt], device="cuda") if r == root else None
             fused = bool(flags & mm.MM_GATHER_C_FUSED)
             mm.gemm_sharded(m, n, p, TORCH_IN[dt], Ad, Bd, None if fused else Cl, layout=mm.MM_ROW_BLOCK,
                             flags=flags, root=root, C_full=Cf)
@@ -102,6 +109,12 @@ def row_block_small(G, r, checks):
                 ok &= np.array_equal(Cf.cpu().numpy().astype(np.float64), Cref)
             if flags & mm.MM_BCAST_B:
                 ok &= torch.equal(Bd.cpu(), to_dev(B, dt).cpu())
+            if win is not None:
+                ok &= bool((win[0] == -9).all() and (win[m + 1] == -9).all())
+                if r != root:  # peers stored into the root's window only
+                    ok &= bool((Cf == -9).all())
+                dist.barrier()
+                mm.window_free(win)
             checks.append({"what": f"row-block {dt} {m}x{n}x{p} flags={flags} root={root}", "ok": allreduce_ok(ok)})
 
 

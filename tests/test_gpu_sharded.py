@@ -155,3 +155,55 @@ def test_collective_argument_check(pg):
     finally:
         os.environ.pop("MM_CHECK_COLLECTIVE", None)
     assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
+
+
+def test_row_block_fused_gather_window_world1(pg):
+    """MM_GATHER_C_FUSED | MM_C_WINDOW: C_full is NCCL symmetric memory
+    (mm_window_alloc: ncclMemAlloc + ncclCommWindowRegister) and the root's address comes from the
+    window (ncclGetPeerPointer) instead of a CUDA-IPC handle exchange.  At world size 1 the root
+    is this rank; the window, its device-side descriptor and the products' TMA stores through the
+    resolved address all run for real.  C_full sits at an offset inside the window (symmetric)."""
+    import paper_2408_15384_b200 as mm
+    m, n, p = 1000, 512, 776
+    for dt in ("bf16", "i8", "f64"):
+        if dt == "bf16":
+            A, B = sg.exact_bf16(37, 1, 9, m, n), sg.exact_bf16(37, 2, 9, n, p)
+            tA = torch.from_numpy(A.view(np.int16)).view(torch.bfloat16).cuda()
+            tB = torch.from_numpy(B.view(np.int16)).view(torch.bfloat16).cuda()
+            Cref, _ = oracle.gemm_bf16(A, B)
+            tdt, odt = torch.bfloat16, torch.float32
+        elif dt == "i8":
+            A, B = sg.exact_i8(37, 1, 255, m, n), sg.exact_i8(37, 2, 255, n, p)
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_s8(A, B)
+            tdt, odt = torch.int8, torch.int32
+        else:
+            A, B = sg.exact_f64(37, 1, 2049, m, n), sg.exact_f64(37, 2, 2049, n, p)
+            tA, tB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+            Cref = oracle.gemm_f64(A, B)
+            tdt, odt = torch.float64, torch.float64
+        win = mm.window_alloc((m + 7, p), odt)
+        try:
+            win.zero_()
+            C_full = win[3:3 + m]
+            flags = mm.MM_GATHER_C_FUSED | mm.MM_C_WINDOW | (mm.MM_BCAST_B if dt != "f64" else 0)
+            mm.gemm_sharded(m, n, p, tdt, tA, tB, None, layout=mm.MM_ROW_BLOCK, flags=flags, root=0,
+                            C_full=C_full)
+            mm.sync_check()
+            assert np.array_equal(C_full.cpu().numpy().astype(np.float64), np.asarray(Cref, np.float64)), dt
+            assert not win[:3].any() and not win[3 + m:].any()
+        finally:
+            mm.window_free(win)
+
+
+def test_window_usage_errors(pg):
+    import paper_2408_15384_b200 as mm
+    t = torch.zeros(64, 64, dtype=torch.float64, device="cuda")
+    with pytest.raises(mm.MMError, match="MM_C_WINDOW applies"):
+        mm.gemm_sharded(64, 64, 64, torch.float64, t, t.clone(), t.clone(), layout=mm.MM_ROW_BLOCK,
+                        flags=mm.MM_C_WINDOW, C_full=t.clone())
+    with pytest.raises(mm.MMError, match="not in a buffer from mm_window_alloc"):
+        mm.gemm_sharded(64, 64, 64, torch.float64, t, t.clone(), None, layout=mm.MM_ROW_BLOCK,
+                        flags=mm.MM_GATHER_C_FUSED | mm.MM_C_WINDOW, C_full=t.clone())
+    with pytest.raises(mm.MMError, match="was not returned by mm_window_alloc"):
+        mm.window_free(t)
