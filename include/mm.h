@@ -13,6 +13,15 @@
  * Types (mm_dtype, input → output):
  *   MM_F64      double   × double   → double   (the paper's precision)
  *   MM_BF16_F32 bfloat16 × bfloat16 → float    (FP32 accumulate; BASELINE.json config 3)
+ *   MM_F64_EMU  double   × double   → double   (the same binary64 product computed on the INT8
+ *                                               tensor cores: exact 7-bit digit slices of A rows /
+ *                                               B columns, 36 exact INT8·INT8→INT32 products,
+ *                                               power-of-two scaling, binary64 accumulation
+ *                                               (Ozaki scheme); exact for integer inputs below 2^14,
+ *                                               ~1e-16 normalised error on U[-1,1) inputs; n must
+ *                                               keep 4·n·127² < 2^31 per INT32 sum (n ≤ 33280);
+ *                                               device scratch ≈ 16·n·(m+p)/2 + 4·m·p bytes; plain
+ *                                               products only, not for mm_gemm_sharded)
  *   MM_S8_S32   int8     × int8     → int32    (INT32 accumulate, exact while
  *                                               n·128² < 2^31; BASELINE.json config 2)
  *
@@ -43,7 +52,7 @@
 extern "C" {
 #endif
 
-typedef enum { MM_F64 = 0, MM_BF16_F32 = 1, MM_S8_S32 = 2 } mm_dtype;
+typedef enum { MM_F64 = 0, MM_BF16_F32 = 1, MM_S8_S32 = 2, MM_F64_EMU = 3 } mm_dtype;
 
 typedef enum {
   MM_OK = 0,

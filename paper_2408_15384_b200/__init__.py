@@ -18,17 +18,17 @@ import threading
 import torch
 
 from . import _lib
-from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_C_WINDOW, MM_F64, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE,
-                   MM_ROW_BLOCK, MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
+from ._lib import (MM_BCAST_B, MM_BF16_F32, MM_C_WINDOW, MM_F64, MM_F64_EMU, MM_GATHER_C, MM_GATHER_C_FUSED,
+                   MM_REPLICATE, MM_ROW_BLOCK, MM_S8_S32, MM_SUMMA_2D, MM_SUMMA_25D)
 
 __all__ = ["gemm", "gemm_host", "gemm_sharded", "shard_range", "summa_panels", "shard_plan", "workspace_size",
            "ipc_export", "ipc_open", "window_alloc", "window_free", "clock_meter", "MMError", "Context",
            "sync_check", "version", "launches", "MM_F64", "MM_BF16_F32", "MM_S8_S32", "MM_ROW_BLOCK", "MM_SUMMA_2D",
            "MM_BCAST_B", "MM_GATHER_C", "MM_GATHER_C_FUSED", "MM_REPLICATE", "MM_SUMMA_25D",
-           "MM_C_WINDOW"]
+           "MM_C_WINDOW", "MM_F64_EMU"]
 
 IN_DTYPE = {torch.float64: MM_F64, torch.bfloat16: MM_BF16_F32, torch.int8: MM_S8_S32}
-OUT_DTYPE = {MM_F64: torch.float64, MM_BF16_F32: torch.float32, MM_S8_S32: torch.int32}
+OUT_DTYPE = {MM_F64: torch.float64, MM_BF16_F32: torch.float32, MM_S8_S32: torch.int32, MM_F64_EMU: torch.float64}
 
 
 class MMError(RuntimeError):
@@ -112,9 +112,14 @@ except AttributeError:  # pragma: no cover
 
 
 def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
-         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """C = A·B on the GPU (async on `stream`, default: torch's current stream)."""
+         stream: torch.cuda.Stream | None = None, f64_emulation: bool = False) -> torch.Tensor:
+    """C = A·B on the GPU (async on `stream`, default: torch's current stream).
+    f64_emulation (float64 operands): MM_F64_EMU, the binary64 product on the INT8 tensor cores."""
     m, n, p, dt = _check_operands(A, B)
+    if f64_emulation:
+        if dt != MM_F64:
+            raise ValueError("f64_emulation needs float64 operands")
+        dt = MM_F64_EMU
     dev = A.device
     if dev.type != "cuda" or B.device != dev:
         raise ValueError("gemm expects A and B on the same CUDA device (use gemm_host for host operands)")

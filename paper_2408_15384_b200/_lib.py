@@ -9,7 +9,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MM_B200_LIB") or os.path.join(_HERE, "libmm_b200.so")  # override: A/B builds
 
-MM_F64, MM_BF16_F32, MM_S8_S32 = 0, 1, 2
+MM_F64, MM_BF16_F32, MM_S8_S32, MM_F64_EMU = 0, 1, 2, 3
 MM_OK, MM_ERR_RUNTIME, MM_ERR_USAGE, MM_ERR_UNSUPPORTED, MM_ERR_WORKSPACE = 0, 1, 2, 3, 4
 MM_ROW_BLOCK, MM_SUMMA_2D, MM_SUMMA_25D = 0, 1, 2
 MM_BCAST_B, MM_GATHER_C, MM_GATHER_C_FUSED, MM_REPLICATE, MM_C_WINDOW = 1, 2, 4, 8, 16

@@ -60,6 +60,8 @@ struct mm_ctx {
     void* comm;  // ncclComm_t it is registered with
   };
   std::vector<Window> windows;
+  void* emu_buf = nullptr;    // MM_F64_EMU: digit planes of A and B, INT32 partial product, exponents
+  size_t emu_bytes = 0;
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   unsigned long long* clk_buf = nullptr;  // clock meter: 4096 CTAs x {c0, t0, c1, t1} of the last launch
@@ -106,5 +108,9 @@ mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need);
 mm_status refuse_diag_knobs(mm_ctx* ctx);
 mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s);
+// MM_F64_EMU (f64_emu.cu): binary64 product on the INT8 tensor cores (exact digit slices)
+mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const double* A, int64_t lda, const double* B,
+                       int64_t ldb, double* C, int64_t ldc, int beta_one, cudaStream_t s);
+size_t f64_emu_scratch(int64_t m, int64_t n, int64_t p);
 
 }  // namespace mmb

@@ -31,8 +31,8 @@ mm_status set_err(mm_ctx* ctx, mm_status s, const char* fmt, ...) {
   return s;
 }
 
-size_t dtype_in_size(mm_dtype t) { return t == MM_F64 ? 8 : (t == MM_BF16_F32 ? 2 : 1); }
-size_t dtype_out_size(mm_dtype t) { return t == MM_F64 ? 8 : 4; }
+size_t dtype_in_size(mm_dtype t) { return (t == MM_F64 || t == MM_F64_EMU) ? 8 : (t == MM_BF16_F32 ? 2 : 1); }
+size_t dtype_out_size(mm_dtype t) { return (t == MM_F64 || t == MM_F64_EMU) ? 8 : 4; }
 
 mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need) {
   if (*have >= need && *buf) return MM_OK;
@@ -216,6 +216,9 @@ mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, 
 
 mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
                        const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s) {
+  if (dtype == MM_F64_EMU)
+    return gemm_f64_emu(ctx, m, n, p, static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb,
+                        static_cast<double*>(C), ldc, beta_one, s);
   const size_t esz = dtype_in_size(dtype);
   // persistent grids over the SMs not reserved for concurrent (communication) kernels
   const int num_sms = std::max(4, (ctx->num_sms - std::max(0, ctx->sm_reserve)) & ~1);
@@ -534,7 +537,7 @@ using namespace mmb;
 static mm_status validate(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, const void* B,
                           const void* C) {
   if (!ctx) return MM_ERR_USAGE;
-  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32)
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32 && dtype != MM_F64_EMU)
     return set_err(ctx, MM_ERR_USAGE, "unknown dtype %d", (int)dtype);
   if (m < 1 || n < 1 || p < 1)
     return set_err(ctx, MM_ERR_USAGE, "dimensions must be >= 1: A is %lld x %lld, B is %lld x %lld", (long long)m,
@@ -621,6 +624,7 @@ __attribute__((visibility("default"))) void mm_destroy(mm_ctx* ctx) {
   if (ctx->sk_flags) cudaFree(ctx->sk_flags);
   if (ctx->trace_buf) cudaFree(ctx->trace_buf);
   if (ctx->clk_buf) cudaFree(ctx->clk_buf);
+  if (ctx->emu_buf) cudaFree(ctx->emu_buf);
   for (auto& b : ctx->hbuf)
     if (b) cudaFree(b);
   for (auto& b : ctx->sbuf)
@@ -667,6 +671,10 @@ int64_t product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
 __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                                                                  mm_layout layout, int G) {
   if (m < 1 || n < 1 || p < 1 || G < 1) return 0;
+  if (dtype == MM_F64_EMU)  // plain products only: digit planes + INT32 partial + the INT8 product's own scratch
+    return (layout == MM_ROW_BLOCK && G == 1)
+               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, 4 * ((n + 15) / 16 * 16), p, MM_S8_S32)
+               : 0;
   if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return 0;
   if (layout != MM_ROW_BLOCK && layout != MM_SUMMA_2D && layout != MM_SUMMA_25D) return 0;
   if (layout != MM_ROW_BLOCK && dtype != MM_F64) return 0;

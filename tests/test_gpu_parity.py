@@ -785,3 +785,34 @@ def test_n_half_tail_same_bits_as_whole_tiles(mm, dt):
     assert torch.equal(outs["0"], outs["4"])
     Cref, D = ref(dt, A[:64], B)
     check(dt, outs["4"][:64].cpu().numpy(), Cref, D, exact=False)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 256), (2000, 1500, 1750), (1000, 333, 517), (37, 4100, 29), (1, 1, 1)])
+def test_f64_emulation(mm, shape):
+    """MM_F64_EMU (f64_emu.cu): the binary64 product on the INT8 tensor cores via exact 7-bit digit
+    slices.  Exact-integer inputs (|x| <= 1024, K = 2049 pins) bit-exact — every digit product and
+    every scaled partial sum is exact; U[-1,1) inputs within the FP64 tolerance of the oracle and,
+    diagnostically, of DMMA's ~1e-16; ragged n (K padding) and p % 4 != 0 (byte digit stores)."""
+    m, n, p = shape
+    A, B = gen("f64", "exact", 71, m, n, p, 2049)
+    Cref, _ = ref("f64", A, B)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    assert np.array_equal(C.cpu().numpy(), Cref)
+    A, B = gen("f64", "random", 72, m, n, p)
+    Cref, D = ref("f64", A, B)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    err = oracle.normalized_error(C.cpu().numpy(), Cref, D)
+    assert err <= TOL["f64"], err
+    assert err <= 1e-15, f"diagnostic: emulation error {err} well above DMMA's"
+
+
+def test_f64_emulation_config1_golden(mm):
+    """C2x (configs[1] shape, K=2049 exact pin): the emulated product's full-output checksum equals
+    SURVEY c7's golden, like DMMA's."""
+    m, n, p = 2000, 1500, 1750
+    A, B = gen("f64", "exact", 1, m, n, p, 2049)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    assert sg.checksum(C.cpu().numpy()) == int(FULL["C2x"]["checksum"], 16)
