@@ -453,6 +453,23 @@ def per_config_table(mm, peaks, k6=None):
                 "cublas_ms": round(t_ref, 4), "cublas_tflops": round(flops / t_ref / 1e9, 2),
                 "l2": "flushed before each launch" if not big else "operands larger than L2",
             }
+            if dt == "f64" and m >= 1024:
+                # MM_F64_EMU: the same binary64 product on the INT8 tensor cores (exact digit slices,
+                # DESIGN §6) — reported beside the DMMA default, with its difference from DMMA's output
+                t_emu = per_launch_ms(lambda: mm.gemm(A, B, out=C, f64_emulation=True), max(2, reps // 2),
+                                      None if big else flush)
+                C2 = torch.empty_like(C)
+                mm.gemm(A, B, out=C2)
+                mm.gemm(A, B, out=C, f64_emulation=True)
+                mm.sync_check()
+                rel = ((C - C2).abs().max() / (A.abs().max() * B.abs().max() * n)).item()
+                del C2
+                out[name]["f64_emulation"] = {
+                    "ms": round(t_emu, 4), "tflops": round(flops / t_emu / 1e9, 2),
+                    "vs_cublas_dgemm": round(t_ref / t_emu, 3),
+                    "max_abs_diff_vs_dmma_over_n_maxA_maxB": rel,
+                    "how": "mm.gemm(..., f64_emulation=True) = MM_F64_EMU: 8 exact 7-bit digit slices per "
+                           "row of A / column of B, 36 INT8 tcgen05 products (INT32 exact), binary64 accumulation"}
             del A, B, C
             torch.cuda.empty_cache()
         except Exception as e:  # noqa: BLE001

@@ -816,3 +816,37 @@ def test_f64_emulation_config1_golden(mm):
     C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
     mm.sync_check()
     assert sg.checksum(C.cpu().numpy()) == int(FULL["C2x"]["checksum"], 16)
+
+
+def test_config4_fp64_32768_emulated(mm):
+    """configs[4] at full size through MM_F64_EMU: the C5x exact pin (K=2049 integers; every digit
+    product, scaled partial and sum exact) hashes to the oracle's golden bit for bit; random U[-1,1)
+    inputs match the oracle on >= 64 seeded rows and >= 64 seeded columns (+ seams) within 1e-12,
+    and diagnostically within 1e-15."""
+    from synthgen import gpu as sgg
+    N = 32768
+    A = sgg.exact_f64(4, sg.ROLE_A, 2049, N, N)
+    B = sgg.exact_f64(4, sg.ROLE_B, 2049, N, N)
+    C = mm.gemm(A, B, f64_emulation=True)
+    mm.sync_check()
+    del A, B
+    Ch = C.cpu().numpy()
+    del C
+    torch.cuda.empty_cache()
+    assert sg.checksum(Ch) == int(FULL["C5x"]["checksum"], 16)
+    del Ch
+    A, B = gen("f64", "random", 4, N, N, N)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    rows = _sample(N, 64, 3, 4, [0, N - 1, 16383, 16384])
+    cols = _sample(N, 64, 4, 4, [0, N - 1, 8191, 8192])
+    Crow = C[torch.from_numpy(rows).cuda()].cpu().numpy()
+    Ccol = C[:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    del C
+    torch.cuda.empty_cache()
+    Cr, Dr = oracle.gemm_f64_rows(A, B, rows)
+    Cc, Dc = oracle.gemm_f64_cols(A, B, cols)
+    for got, want, D in ((Crow, Cr, Dr), (Ccol, Cc, Dc)):
+        err = oracle.normalized_error(got, want, D)
+        assert err <= TOL["f64"], err
+        assert err <= 1e-15, f"diagnostic: {err}"
