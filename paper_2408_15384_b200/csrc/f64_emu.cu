@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kDigits = 8;           // S: 8 x 7 bits = 56 >= 53
 constexpr int kExpBias = 4096;       // encoded exponent (0 = all-zero row / column)
-constexpr int64_t kMaxPairs = 4;     // INT8 products summed in one INT32 accumulator
+constexpr int64_t kMaxPairs = 8;     // INT8 products summed in one INT32 accumulator (n permitting)
 
 __device__ __forceinline__ int dec_exp(int v) { return v ? v - kExpBias : 0; }
 

@@ -673,7 +673,7 @@ __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64
   if (m < 1 || n < 1 || p < 1 || G < 1) return 0;
   if (dtype == MM_F64_EMU)  // plain products only: digit planes + INT32 partial + the INT8 product's own scratch
     return (layout == MM_ROW_BLOCK && G == 1)
-               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, 4 * ((n + 15) / 16 * 16), p, MM_S8_S32)
+               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, 8 * ((n + 15) / 16 * 16), p, MM_S8_S32)
                : 0;
   if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return 0;
   if (layout != MM_ROW_BLOCK && layout != MM_SUMMA_2D && layout != MM_SUMMA_25D) return 0;
