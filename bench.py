@@ -359,6 +359,17 @@ def compulsory_bytes(dt, m, n, p):
     return (m * n + n * p) * ei + m * p * eo
 
 
+def emu_plan(n):
+    """MM_F64_EMU's moduli and scaling width for inner dimension n (mm_f64_emu_plan, host logic)."""
+    import ctypes
+
+    from paper_2408_15384_b200 import _lib
+    mods, cnt, beta = (ctypes.c_int * 16)(), ctypes.c_int(), ctypes.c_int()
+    if _lib.load().mm_f64_emu_plan(n, mods, ctypes.byref(cnt), ctypes.byref(beta)) != 0:
+        return None
+    return {"count": cnt.value, "beta": beta.value, "moduli": list(mods[:cnt.value])}
+
+
 def per_config_table(mm, peaks, k6=None):
     """Brief timings of the other BASELINE.json configs at N=1 (ours vs cuBLAS)."""
     import torch
@@ -454,8 +465,8 @@ def per_config_table(mm, peaks, k6=None):
                 "l2": "flushed before each launch" if not big else "operands larger than L2",
             }
             if dt == "f64" and m >= 1024:
-                # MM_F64_EMU: the same binary64 product on the INT8 tensor cores (exact digit slices,
-                # DESIGN §6) — reported beside the DMMA default, with its difference from DMMA's output
+                # MM_F64_EMU: the same binary64 product on the INT8 tensor cores (Ozaki scheme II,
+                # DESIGN §6 K5) — reported beside the DMMA default, with its difference from DMMA's output
                 t_emu = per_launch_ms(lambda: mm.gemm(A, B, out=C, f64_emulation=True), max(2, reps // 2),
                                       None if big else flush)
                 C2 = torch.empty_like(C)
@@ -468,8 +479,10 @@ def per_config_table(mm, peaks, k6=None):
                     "ms": round(t_emu, 4), "tflops": round(flops / t_emu / 1e9, 2),
                     "vs_cublas_dgemm": round(t_ref / t_emu, 3),
                     "max_abs_diff_vs_dmma_over_n_maxA_maxB": rel,
-                    "how": "mm.gemm(..., f64_emulation=True) = MM_F64_EMU: 8 exact 7-bit digit slices per "
-                           "row of A / column of B, 36 INT8 tcgen05 products (INT32 exact), binary64 accumulation"}
+                    "moduli": emu_plan(n),
+                    "how": "mm.gemm(..., f64_emulation=True) = MM_F64_EMU: rows of A / columns of B scaled to "
+                           "integers of >= 53 bits, one exact INT8 tcgen05 product (INT32) per coprime modulus, "
+                           "Chinese remaindering, one rounding to binary64"}
             del A, B, C
             torch.cuda.empty_cache()
         except Exception as e:  # noqa: BLE001

@@ -14,14 +14,19 @@
  *   MM_F64      double   × double   → double   (the paper's precision)
  *   MM_BF16_F32 bfloat16 × bfloat16 → float    (FP32 accumulate; BASELINE.json config 3)
  *   MM_F64_EMU  double   × double   → double   (the same binary64 product computed on the INT8
- *                                               tensor cores: exact 7-bit digit slices of A rows /
- *                                               B columns, 36 exact INT8·INT8→INT32 products,
- *                                               power-of-two scaling, binary64 accumulation
- *                                               (Ozaki scheme); exact for integer inputs below 2^14,
- *                                               ~1e-16 normalised error on U[-1,1) inputs; n must
- *                                               keep 4·n·127² < 2^31 per INT32 sum (n ≤ 33280);
- *                                               device scratch ≈ 16·n·(m+p)/2 + 4·m·p bytes; plain
- *                                               products only, not for mm_gemm_sharded)
+ *                                               tensor cores (Ozaki scheme, second kind): rows of A
+ *                                               / columns of B scaled by powers of two to integers
+ *                                               of β ≥ 53 bits, their residues modulo N = 14..16
+ *                                               coprime moduli ≤ 256 multiplied as N exact
+ *                                               INT8·INT8→INT32 products, the integer product
+ *                                               rebuilt by Chinese remaindering (Garner) and
+ *                                               rounded once to binary64; exact for integer
+ *                                               inputs, ~1e-17..1e-16 normalised error on U[-1,1)
+ *                                               inputs; finite inputs only; n < 131072 (n·2^14 <
+ *                                               2^31 per INT32 sum); device scratch ≈
+ *                                               N·(m·n + n·p + m·p) + 4·m·p bytes
+ *                                               (mm_workspace_size); plain products only, not for
+ *                                               mm_gemm_sharded)
  *   MM_S8_S32   int8     × int8     → int32    (INT32 accumulate, exact while
  *                                               n·128² < 2^31; BASELINE.json config 2)
  *
@@ -265,6 +270,13 @@ mm_status mm_shard_plan(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layo
  * internal padding buffer.  Pure host logic: the bound assumes at most 160 SMs.  0 for invalid
  * arguments. */
 size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layout layout, int G);
+
+/* MM_F64_EMU plan for inner dimension n (pure host logic): writes the moduli used (the first
+ * *count of the fixed list, largest first, pairwise coprime, each ≤ 256) to `moduli` (room for 16;
+ * may be NULL) and the scaling width β to *beta: the fewest moduli with
+ * n·2^(2β) ≤ Π m_l / 2 − 1 and β ≥ 53, β as large as that product allows (≤ 60).
+ * MM_ERR_USAGE for n < 1, null count/beta; MM_ERR_UNSUPPORTED for n ≥ 131072 (INT32 sums). */
+mm_status mm_f64_emu_plan(int64_t n, int* moduli, int* count, int* beta);
 
 /* Clock meter (measurement): enable = 1 makes every product kernel of this context record, per
  * CTA, its SM cycle count (clock64) and elapsed nanoseconds (globaltimer) between entry and exit

@@ -19,7 +19,7 @@ EXPORTS = (
     "mm_create", "mm_destroy", "mm_gemm", "mm_gemm_host", "mm_sync_check", "mm_status_string",
     "mm_last_error", "mm_gemm_sharded", "mm_shard_range", "mm_summa_panels", "mm_launches", "mm_version",
     "mm_shard_plan", "mm_workspace_size", "mm_ipc_export", "mm_ipc_open", "mm_clock_meter",
-    "mm_window_alloc", "mm_window_free",
+    "mm_window_alloc", "mm_window_free", "mm_f64_emu_plan",
 )
 
 # mm_plan_op / mm_plan_buf / mm_plan_comm (include/mm.h)
@@ -97,6 +97,8 @@ def load():
     lib.mm_window_free.restype = _int
     lib.mm_clock_meter.argtypes = [_vp, _int, ctypes.POINTER(ctypes.c_double)]
     lib.mm_clock_meter.restype = _int
+    lib.mm_f64_emu_plan.argtypes = [_i64, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_int)]
+    lib.mm_f64_emu_plan.restype = _int
     lib.mm_version.argtypes = []
     lib.mm_version.restype = ctypes.c_char_p
     _lib = lib

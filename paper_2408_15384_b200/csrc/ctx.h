@@ -108,9 +108,13 @@ mm_status ensure_buffer(mm_ctx* ctx, void** buf, size_t* have, size_t need);
 mm_status refuse_diag_knobs(mm_ctx* ctx);
 mm_status gemm_ld(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dtype, const void* A, int64_t lda,
                   const void* B, int64_t ldb, void* C, int64_t ldc, int beta_one, cudaStream_t s);
-// MM_F64_EMU (f64_emu.cu): binary64 product on the INT8 tensor cores (exact digit slices)
+// MM_F64_EMU (f64_emu.cu): binary64 product on the INT8 tensor cores (integer scaling, residues modulo
+// N coprime moduli, N exact INT8 products, Chinese remaindering)
 mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const double* A, int64_t lda, const double* B,
                        int64_t ldb, double* C, int64_t ldc, int beta_one, cudaStream_t s);
 size_t f64_emu_scratch(int64_t m, int64_t n, int64_t p);
+int64_t f64_emu_max_n();
+// moduli count N (0: none) and β for inner dimension n; the moduli themselves into mods (room for 16)
+int f64_emu_moduli(int64_t n, int* beta, int* mods);
 
 }  // namespace mmb

@@ -1,23 +1,28 @@
 // f64_emu.cu — MM_F64_EMU: the binary64 product C = A·B (the paper's `double`
-// precision) computed on the INT8 tensor cores by exact digit slicing (the Ozaki
-// scheme), for problems where the 2.25 / 4.5 PFLOP/s tensor pipes beat the 37 TFLOP/s DMMA pipe.
+// precision) computed on the INT8 tensor cores by exact modular arithmetic (the
+// Ozaki scheme, second kind: integer scaling + Chinese remaindering), for problems where the
+// 4.5 POPS INT8 pipe beats the 37 TFLOP/s DMMA pipe.
 //
-//   * Row i of A is scaled by 2^-e_i (|a_ik| < 2^e_i, e_i the frexp exponent of the row maximum)
-//     and each scaled element x ∈ (-1, 1) is cut into S = 8 signed 7-bit digits
-//     x = Σ_u d_u 2^(-7u), d_u = trunc(128 · remainder) ∈ [-127, 127] — exact in binary64 (a
-//     multiplication by 2^7 and the subtraction of an integer part are exact), 56 bits ≥ 53.
-//     Column j of B likewise with 2^-f_j into digits g_v.
-//   * a_ik·b_kj summed over k = Σ_{u,v} 2^(e_i + f_j - 7(u+v)) Σ_k d_u,ik g_v,kj; each inner sum is
-//     an INT8 product with INT32 accumulation, exact while (#pairs)·n·127² < 2^31 (n ≤ 33288 for 4
-//     pairs — C5's n = 32768 fits 4).  Pairs of equal weight w = u+v are one INT8 GEMM whose K
-//     runs over the pairs: A digits stored [row][u][k], B digits [8-v][k][col], so the pairs of a
-//     weight are contiguous K ranges of both (no copy).  Pairs with w ≤ S+1 (36 of 64) are kept; the
-//     dropped ones weigh ≤ 2^(-70) relative to the row/column scales.
-//   * Each weight's INT32 result is scaled by the exact power of two and added into C in binary64,
-//     smallest weights first (fixed order: run-to-run identical).
-// Accuracy: exact integer inputs (|x| < 2^14) give exact results (bit-identical to the oracle);
-// U[-1,1) inputs give normalised errors ~1e-16, like DMMA (tests/test_gpu_parity.py).
+//   * Integer scaling.  Row i of A is scaled by 2^(β - e_i) (e_i = frexp exponent of the row
+//     maximum, so |·| < 2^β) and rounded: a'_ik = rint(a_ik · 2^(β-e_i)), an exact binary64
+//     integer with |a'| ≤ 2^β; column j of B likewise with 2^(β-f_j) into b'_kj.  The rounding
+//     error is ≤ 2^-β of the row / column maximum (β ≥ 53: the binary64 rounding of that maximum);
+//     an integer input stays an integer after the scaling (2^(β-e) ≥ 1), so it is not rounded.
+//   * Residues.  N pairwise-coprime moduli m_1..m_N ≤ 256 (M = Π m_l); the symmetric residues
+//     a'_ik mod m_l, b'_kj mod m_l lie in [-128, 127], so each C'_l = A'_l · B'_l is one INT8
+//     product with INT32 accumulation, exact while n · 2^14 < 2^31 (n < 131072).
+//   * Reconstruction.  C' = A'·B' is an integer with |C'| ≤ n · 2^(2β); N and β are chosen so that
+//     n · 2^(2β) ≤ M/2 - 1 with β ≥ 53 (N = 14..16 for n < 131072).  Garner's algorithm turns the
+//     residues c_l = C'_l mod m_l into symmetric mixed-radix digits v_l (exact small-integer
+//     arithmetic), C' = v_1 + m_1 (v_2 + m_2 (v_3 + ...)), evaluated by Horner's rule in
+//     double-double (exact while below 2^106 relative error), rounded once to binary64 and scaled
+//     by 2^-(2β - e_i - f_j) (exact unless the result is subnormal).
+// Accuracy: exact integer inputs give exact results (bit-identical to the oracle); U[-1,1) inputs
+// give normalised errors ~1e-17..1e-16, the accuracy class of DMMA (tests/test_gpu_parity.py).
+// Inputs must be finite.  Cost: N INT8 GEMMs (16 at C5) instead of DMMA's n/4 DMMA k-steps.
+#include <cfloat>
 #include <climits>
+#include <cmath>
 #include <cstdint>
 
 #include "ctx.h"
@@ -27,11 +32,92 @@ namespace mmb {
 
 namespace {
 
-constexpr int kDigits = 8;           // S: 8 x 7 bits = 56 >= 53
-constexpr int kExpBias = 4096;       // encoded exponent (0 = all-zero row / column)
-constexpr int64_t kMaxPairs = 8;     // INT8 products summed in one INT32 accumulator (n permitting)
+constexpr int kMaxMod = 16;   // moduli used at most (n < 131072 needs at most 16 for β ≥ 53)
+constexpr int kMinMod = 14;   // fewest moduli that give β ≥ 53 at n = 1
+constexpr int kMinBeta = 53;  // bits kept of every row / column maximum
+constexpr int kMaxBeta = 60;
+constexpr int kExpBias = 4096;  // encoded exponent (0 = all-zero row / column)
+// pairwise coprime, largest first (256 = 2^8, 255 = 3·5·17, 253 = 11·23, 247 = 13·19, 217 = 7·31,
+// the rest prime)
+constexpr int kMods[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+// Garner tables, passed by value (kernel parameter space: constant-bank operands)
+struct CrtTab {
+  int nmod;                       // N
+  int beta;                       // β
+  int m[kMaxMod];                 // m_l
+  float rcp[kMaxMod];             // 1/m_l (rounded; the reductions correct the quotient)
+  double rcpd[kMaxMod];           // 1/m_l in binary64
+  // 0-based digits: C' = Σ_q v_q P_q with P_0 = 1, P_q = m[0] ... m[q-1]
+  int pmod[kMaxMod][kMaxMod];     // pmod[q][k] = P_q mod m[k] for q < k
+  int pinv[kMaxMod];              // (P_k mod m[k])^-1 mod m[k]
+};
+
+int inv_mod(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
+  int t = 0, nt = 1, r = m, nr = ((a % m) + m) % m;
+  while (nr) {
+    const int q = r / nr;
+    int x = t - q * nt; t = nt; nt = x;
+    x = r - q * nr; r = nr; nr = x;
+  }
+  return ((t % m) + m) % m;
+}
+
+// N and β for inner dimension n: the fewest moduli with β = floor((log2 M - 1 - log2 n) / 2) ≥ 53
+bool crt_plan(int64_t n, int* nmod, int* beta) {
+  double lm = 0.0;
+  for (int l = 0; l < kMaxMod; ++l) {
+    lm += std::log2((double)kMods[l]);
+    if (l + 1 < kMinMod) continue;
+    const double room = lm - 1.0 - std::log2((double)n) - 1e-9;
+    const int b = (int)std::floor(room / 2.0);
+    if (b >= kMinBeta) {
+      *nmod = l + 1;
+      *beta = std::min(b, kMaxBeta);
+      return true;
+    }
+  }
+  return false;
+}
+
+CrtTab make_tab(int nmod, int beta) {
+  CrtTab t{};
+  t.nmod = nmod;
+  t.beta = beta;
+  for (int l = 0; l < kMaxMod; ++l) {
+    t.m[l] = kMods[l];
+    t.rcp[l] = 1.0f / (float)kMods[l];
+    t.rcpd[l] = 1.0 / (double)kMods[l];
+  }
+  for (int k = 0; k < kMaxMod; ++k) {
+    int pk = 1 % kMods[k];  // P_0 mod m[k]
+    for (int j = 0; j < k; ++j) {
+      t.pmod[j][k] = pk;  // P_j mod m[k]
+      pk = (int)((int64_t)pk * kMods[j] % kMods[k]);
+    }
+    t.pinv[k] = k == 0 ? 1 : inv_mod(pk, kMods[k]);  // pk = P_k mod m[k]
+  }
+  return t;
+}
 
 __device__ __forceinline__ int dec_exp(int v) { return v ? v - kExpBias : 0; }
+
+// x mod m in [0, m) for |x| < 2^24 (float quotient, corrected)
+__device__ __forceinline__ int mod_small(int x, int m, float rcp) {
+  const int q = __float2int_rd(__int2float_rn(x) * rcp);
+  int r = x - q * m;
+  r += r < 0 ? m : 0;
+  r -= r >= m ? m : 0;
+  return r;
+}
+
+// symmetric residue in [-128, 127] of an integer-valued binary64 |x| < 2^62
+__device__ __forceinline__ int sym_residue(double x, int m, double rcpd, float rcp) {
+  const double q = floor(x * rcpd);
+  const int r0 = (int)fma(-q, (double)m, x);  // exact: |x - q m| < 8 m
+  int r = mod_small(r0, m, rcp);
+  return r > (m >> 1) - (m & 1 ? 0 : 1) ? r - m : r;  // odd m: [-(m-1)/2, (m-1)/2]; 256: [-128, 127]
+}
 
 // e[i] = bias + frexp exponent of max_k |A[i][k]| (0 if the row is zero)
 __global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int* __restrict__ e) {
@@ -68,75 +154,113 @@ __global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_
   }
 }
 
-// 8 digits of x ∈ (-1, 1): d_u = trunc(128 r_{u-1}), r_u = 128 r_{u-1} - d_u (exact)
-__device__ __forceinline__ void digits(double x, int (&d)[kDigits]) {
+// A residue planes: Ar[(l*m + i)*kp + k] = a'_ik mod m_l (k >= n: 0); 4 consecutive k per thread
+template <int N>
+__global__ void residues_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t kp,
+                                  const int* __restrict__ e, int8_t* __restrict__ Ar, const __grid_constant__ CrtTab t) {
+  const int64_t q4 = kp / 4;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * q4; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = w / q4, k0 = (w % q4) * 4;
+    const int sc = t.beta - dec_exp(e[i]);
+    double x[4];
 #pragma unroll
-  for (int u = 0; u < kDigits; ++u) {
-    x *= 128.0;
-    const double t = trunc(x);
-    d[u] = (int)t;
-    x -= t;
+    for (int c = 0; c < 4; ++c) x[c] = k0 + c < n ? rint(ldexp(A[i * lda + k0 + c], sc)) : 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        word |= (uint32_t)(uint8_t)(int8_t)sym_residue(x[c], t.m[l], t.rcpd[l], t.rcp[l]) << (8 * c);
+      *reinterpret_cast<uint32_t*>(Ar + ((int64_t)l * m + i) * kp + k0) = word;
+    }
   }
 }
 
-// A digits: Ad[(i*8 + u)*kp + k] (k >= n zero); 4 consecutive k per thread, packed 32-bit stores
-__global__ void slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t kp,
-                               const int* __restrict__ e, int8_t* __restrict__ Ad) {
-  const int64_t q4 = kp / 4;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * q4; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / q4, k0 = (t % q4) * 4;
-    const int sc = -dec_exp(e[i]);
-    uint32_t w[kDigits] = {0, 0, 0, 0, 0, 0, 0, 0};
+// B residue planes: Br[(l*n + k)*pp + j] = b'_kj mod m_l (j >= p: 0); 4 consecutive j per thread
+template <int N>
+__global__ void residues_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t p, int64_t pp,
+                                  const int* __restrict__ f, int8_t* __restrict__ Br, const __grid_constant__ CrtTab t) {
+  const int64_t q4 = pp / 4;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n * q4; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = w / q4, j0 = (w % q4) * 4;
+    double x[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int64_t k = k0 + c;
-      int d[kDigits];
-      digits(k < n ? ldexp(A[i * lda + k], sc) : 0.0, d);
-#pragma unroll
-      for (int u = 0; u < kDigits; ++u) w[u] |= ((uint32_t)(uint8_t)(int8_t)d[u]) << (8 * c);
+      const int64_t j = j0 + c;
+      x[c] = j < p ? rint(ldexp(B[k * ldb + j], t.beta - dec_exp(f[j]))) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < kDigits; ++u) *reinterpret_cast<uint32_t*>(Ad + (i * kDigits + u) * kp + k0) = w[u];
-  }
-}
-
-// B digits: Bd[((8-v)*kp + k)*p + j] for digit v = 1..8 (plane 0 holds digit 8); k >= n rows zero.
-// P4: p % 4 == 0 -> 4 consecutive columns per thread, packed 32-bit stores.
-template <bool P4>
-__global__ void slice_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t p, int64_t kp,
-                               const int* __restrict__ f, int8_t* __restrict__ Bd) {
-  const int64_t cw = P4 ? p / 4 : p;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kp * cw; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = t / cw, j0 = (t % cw) * (P4 ? 4 : 1);
-    if constexpr (P4) {
-      uint32_t w[kDigits] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int l = 0; l < N; ++l) {
+      uint32_t word = 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        int d[kDigits];
-        digits(k < n ? ldexp(B[k * ldb + j0 + c], -dec_exp(f[j0 + c])) : 0.0, d);
-#pragma unroll
-        for (int u = 0; u < kDigits; ++u) w[u] |= ((uint32_t)(uint8_t)(int8_t)d[u]) << (8 * c);
-      }
-#pragma unroll
-      for (int u = 0; u < kDigits; ++u)  // digit v = u + 1 -> plane 8 - v = 7 - u
-        *reinterpret_cast<uint32_t*>(Bd + ((int64_t)(kDigits - 1 - u) * kp + k) * p + j0) = w[u];
-    } else {
-      int d[kDigits];
-      digits(k < n ? ldexp(B[k * ldb + j0], -dec_exp(f[j0])) : 0.0, d);
-#pragma unroll
-      for (int u = 0; u < kDigits; ++u) Bd[((int64_t)(kDigits - 1 - u) * kp + k) * p + j0] = (int8_t)d[u];
+      for (int c = 0; c < 4; ++c)
+        word |= (uint32_t)(uint8_t)(int8_t)sym_residue(x[c], t.m[l], t.rcpd[l], t.rcp[l]) << (8 * c);
+      *reinterpret_cast<uint32_t*>(Br + ((int64_t)l * n + k) * pp + j0) = word;
     }
   }
 }
 
-// C (+)= S · 2^(e_i + f_j - 7w); `assign` overwrites (the first weight of a beta = 0 product)
-__global__ void scale_acc_kernel(const int32_t* __restrict__ S, int64_t m, int64_t p, double* __restrict__ C,
-                                 int64_t ldc, const int* __restrict__ e, const int* __restrict__ f, int w, int assign) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * p; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / p, j = t % p;
-    const double v = ldexp((double)S[t], dec_exp(e[i]) + dec_exp(f[j]) - 7 * w);
+// R[i*pp + j] = S[i*pp + j] mod m in [0, m) (S exact INT32 product of the residues), 4 per thread
+__global__ void reduce_mod_kernel(const int4* __restrict__ S, int64_t count4, int m, double rcpd, float rcp,
+                                  uint32_t* __restrict__ R) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < count4; w += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = S[w];
+    const int s[4] = {v.x, v.y, v.z, v.w};
+    uint32_t word = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double q = floor((double)s[c] * rcpd);
+      const int r0 = (int)fma(-q, (double)m, (double)s[c]);  // exact, |r0| < 2m
+      word |= (uint32_t)mod_small(r0, m, rcp) << (8 * c);
+    }
+    R[w] = word;
+  }
+}
+
+// double-double t·m + v (m ≤ 256, |v| ≤ 128): Horner step of the mixed-radix value
+__device__ __forceinline__ void dd_step(double& hi, double& lo, double m, double v) {
+  const double p = hi * m;
+  const double pe = fma(hi, m, -p);  // hi·m = p + pe exactly
+  const double s = p + v;
+  const double bb = s - p;
+  const double se = (p - (s - bb)) + (v - bb);  // p + v = s + se exactly
+  const double l = fma(lo, m, pe + se);
+  hi = s + l;
+  lo = l - (hi - s);
+}
+
+// C[i][j] (+)= 2^-(2β - e_i - f_j) · C'_ij, C' from its residues R_l by Garner + double-double Horner
+template <int N>
+__global__ void crt_combine_kernel(const uint8_t* __restrict__ R, int64_t m, int64_t p, int64_t pp,
+                                   double* __restrict__ C, int64_t ldc, const int* __restrict__ e,
+                                   const int* __restrict__ f, int beta_one, const __grid_constant__ CrtTab t) {
+  const int64_t plane = m * pp;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * p; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = w / p, j = w % p;
+    const uint8_t* r = R + i * pp + j;
+    int v[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      // v_k = (c_k - Σ_{j<k} v_j (P_j mod m_k)) · (P_k mod m_k)^-1 mod m_k, symmetric
+      int x = (int)__ldg(r + k * plane);
+#pragma unroll
+      for (int q = 0; q < k; ++q) x -= v[q] * t.pmod[q][k];
+      const int y = mod_small(x, t.m[k], t.rcp[k]) * t.pinv[k];
+      const int d = mod_small(y, t.m[k], t.rcp[k]);
+      v[k] = d > (t.m[k] >> 1) ? d - t.m[k] : d;  // 256: [-127, 128]; odd: [-(m-1)/2, (m-1)/2]
+    }
+    // C' = v_0 + m_0 (v_1 + m_1 (v_2 + ...)): exact in binary64 while below 2^53 (the top 6
+    // digits: |value| < 2^48), double-double below
+    double hi = (double)v[N - 1], lo = 0.0;
+#pragma unroll
+    for (int k = N - 2; k >= 0; --k) {
+      if (k >= N - 6) hi = fma(hi, (double)t.m[k], (double)v[k]);
+      else dd_step(hi, lo, (double)t.m[k], (double)v[k]);
+    }
+    const int ei = e[i], fj = f[j];
+    const double val = (ei && fj) ? ldexp(hi + lo, dec_exp(ei) + dec_exp(fj) - 2 * t.beta) : 0.0;
     double* c = C + i * ldc + j;
-    *c = assign ? v : *c + v;
+    *c = beta_one ? *c + val : val;
   }
 }
 
@@ -145,70 +269,117 @@ inline int grid_for(int64_t work, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms * 16));
 }
 
+inline size_t up256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct Layout {
+  int nmod, beta;
+  int64_t kp, pp;
+  size_t a_bytes, b_bytes, s_bytes, r_bytes, e_bytes, f_bytes, total;
+};
+
+bool layout_for(int64_t m, int64_t n, int64_t p, Layout* L) {
+  if (!crt_plan(n, &L->nmod, &L->beta)) return false;
+  L->kp = (n + 15) / 16 * 16;
+  L->pp = (p + 15) / 16 * 16;
+  L->a_bytes = up256((size_t)(L->nmod * m * L->kp));
+  L->b_bytes = up256((size_t)(L->nmod * n * L->pp));
+  L->s_bytes = up256((size_t)(m * L->pp * 4));
+  L->r_bytes = up256((size_t)(L->nmod * m * L->pp));
+  L->e_bytes = up256((size_t)m * 4);
+  L->f_bytes = up256((size_t)p * 4);
+  L->total = L->a_bytes + L->b_bytes + L->s_bytes + L->r_bytes + L->e_bytes + L->f_bytes;
+  return true;
+}
+
+template <int N>
+void launch_residues(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n, int64_t p,
+                     const Layout& L, const int* e, const int* f, int8_t* Ar, int8_t* Br, const CrtTab& t, int sms,
+                     cudaStream_t s) {
+  residues_a_kernel<N><<<grid_for(m * (L.kp / 4), sms), 256, 0, s>>>(A, lda, m, n, L.kp, e, Ar, t);
+  residues_b_kernel<N><<<grid_for(n * (L.pp / 4), sms), 256, 0, s>>>(B, ldb, n, p, L.pp, f, Br, t);
+}
+
+template <int N>
+void launch_combine(const uint8_t* R, int64_t m, int64_t p, int64_t pp, double* C, int64_t ldc, const int* e,
+                    const int* f, int beta_one, const CrtTab& t, int sms, cudaStream_t s) {
+  crt_combine_kernel<N><<<grid_for(m * p, sms), 256, 0, s>>>(R, m, p, pp, C, ldc, e, f, beta_one, t);
+}
+
 }  // namespace
 
-int64_t f64_emu_kp(int64_t n) { return (n + 15) / 16 * 16; }
+int64_t f64_emu_max_n() { return (int64_t)INT32_MAX / (128 * 128); }  // n · 2^14 < 2^31
 
 size_t f64_emu_scratch(int64_t m, int64_t n, int64_t p) {
-  const int64_t kp = f64_emu_kp(n);
-  return (size_t)(m * kDigits * kp) + (size_t)(kDigits * kp * p) + (size_t)(m * p * 4) + (size_t)((m + p) * 4) + 4 * 256;
+  Layout L;
+  return layout_for(m, n, p, &L) ? L.total : 0;
+}
+
+int f64_emu_moduli(int64_t n, int* beta, int* mods) {
+  int nm = 0, b = 0;
+  if (!crt_plan(n, &nm, &b)) return 0;
+  if (beta) *beta = b;
+  if (mods)
+    for (int l = 0; l < nm; ++l) mods[l] = kMods[l];
+  return nm;
 }
 
 mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const double* A, int64_t lda, const double* B,
                        int64_t ldb, double* C, int64_t ldc, int beta_one, cudaStream_t s) {
-  const int64_t kp = f64_emu_kp(n);
-  const int64_t lim = (int64_t)INT32_MAX / (int64_t)(127 * 127);  // n x pairs bound for exact INT32 sums
-  if (kp > lim) return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_F64_EMU: n = %lld exceeds the exact-INT32 bound %lld", (long long)n, (long long)lim);
-  const int64_t max_pairs = std::min<int64_t>(kMaxPairs, lim / kp);
-  const size_t bA = (size_t)(m * kDigits * kp), bB = (size_t)(kDigits * kp * p), bS = (size_t)(m * p * 4);
-  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t need = up(bA) + up(bB) + up(bS) + up((size_t)m * 4) + up((size_t)p * 4);
-  mm_status st = ensure_buffer(ctx, &ctx->emu_buf, &ctx->emu_bytes, need);
+  if (n > f64_emu_max_n())
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_F64_EMU: n = %lld exceeds the exact-INT32 bound %lld", (long long)n,
+                   (long long)f64_emu_max_n());
+  Layout L;
+  if (!layout_for(m, n, p, &L))
+    return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_F64_EMU: no modulus set for n = %lld", (long long)n);
+  mm_status st = ensure_buffer(ctx, &ctx->emu_buf, &ctx->emu_bytes, L.total);
   if (st != MM_OK) return st;
   uint8_t* base = static_cast<uint8_t*>(ctx->emu_buf);
-  int8_t* Ad = reinterpret_cast<int8_t*>(base);
-  int8_t* Bd = reinterpret_cast<int8_t*>(base + up(bA));
-  int32_t* S = reinterpret_cast<int32_t*>(base + up(bA) + up(bB));
-  int* e = reinterpret_cast<int*>(base + up(bA) + up(bB) + up(bS));
-  int* f = reinterpret_cast<int*>(base + up(bA) + up(bB) + up(bS) + up((size_t)m * 4));
+  int8_t* Ar = reinterpret_cast<int8_t*>(base);
+  int8_t* Br = reinterpret_cast<int8_t*>(base + L.a_bytes);
+  int32_t* S = reinterpret_cast<int32_t*>(base + L.a_bytes + L.b_bytes);
+  uint8_t* R = base + L.a_bytes + L.b_bytes + L.s_bytes;
+  int* e = reinterpret_cast<int*>(R + L.r_bytes);
+  int* f = reinterpret_cast<int*>(R + L.r_bytes + L.e_bytes);
+  const CrtTab t = make_tab(L.nmod, L.beta);
   const int sms = ctx->num_sms;
-  auto chk = [&](const char* what) -> mm_status {
+  auto chk = [&](const char* what, int kernels) -> mm_status {
     const cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "MM_F64_EMU %s launch failed: %s", what, cudaGetErrorString(ce));
-    ++ctx->launches;
+    ctx->launches += kernels;
     return MM_OK;
   };
-  // scales and digits
+  // scales
   row_exp_kernel<<<(unsigned)m, 256, 0, s>>>(A, lda, n, e);
-  if ((st = chk("row exponents")) != MM_OK) return st;
+  if ((st = chk("row exponents", 1)) != MM_OK) return st;
   if (cudaMemsetAsync(f, 0, (size_t)p * 4, s) != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "MM_F64_EMU memset failed");
   const int64_t rows_per = std::max<int64_t>(64, (n + 63) / 64);
   col_exp_kernel<<<dim3((unsigned)((p + 255) / 256), (unsigned)((n + rows_per - 1) / rows_per)), 256, 0, s>>>(B, ldb, n, p,
                                                                                                            rows_per, f);
-  if ((st = chk("column exponents")) != MM_OK) return st;
-  slice_a_kernel<<<grid_for(m * (kp / 4), sms), 256, 0, s>>>(A, lda, m, n, kp, e, Ad);
-  if ((st = chk("A digits")) != MM_OK) return st;
-  if (p % 4 == 0) slice_b_kernel<true><<<grid_for(kp * (p / 4), sms), 256, 0, s>>>(B, ldb, n, p, kp, f, Bd);
-  else slice_b_kernel<false><<<grid_for(kp * p, sms), 256, 0, s>>>(B, ldb, n, p, kp, f, Bd);
-  if ((st = chk("B digits")) != MM_OK) return st;
-  // weights w = u + v from the smallest (w = S + 1) to the largest (w = 2); each weight's pairs
-  // u = u0..u1 (v = w - u) in chunks of at most max_pairs: one INT8 GEMM over K = chunk x kp
-  bool first = true;
-  for (int w = kDigits + 1; w >= 2; --w) {
-    const int u0 = std::max(1, w - kDigits), u1 = std::min(kDigits, w - 1);
-    for (int ua = u0; ua <= u1; ua += (int)max_pairs) {
-      const int cnt = std::min<int>((int)max_pairs, u1 - ua + 1);
-      const int q0 = kDigits - w + ua;  // B plane of digit v = w - ua
-      const int8_t* Aw = Ad + (int64_t)(ua - 1) * kp;
-      const int8_t* Bw = Bd + (int64_t)q0 * kp * p;
-      st = gemm_ld(ctx, m, cnt * kp, p, MM_S8_S32, Aw, kDigits * kp, Bw, p, S, p, 0, s);
-      if (st != MM_OK) return st;
-      scale_acc_kernel<<<grid_for(m * p, sms), 256, 0, s>>>(S, m, p, C, ldc, e, f, w, (first && !beta_one) ? 1 : 0);
-      if ((st = chk("scale-accumulate")) != MM_OK) return st;
-      first = false;
-    }
+  if ((st = chk("column exponents", 1)) != MM_OK) return st;
+  // residues of the scaled integers
+  switch (L.nmod) {
+    case 14: launch_residues<14>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
+    case 15: launch_residues<15>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
+    default: launch_residues<16>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
   }
-  return MM_OK;
+  if ((st = chk("residues", 2)) != MM_OK) return st;
+  // one exact INT8 product per modulus, reduced to its residue
+  for (int l = 0; l < L.nmod; ++l) {
+    st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp, S, L.pp,
+                 0, s);
+    if (st != MM_OK) return st;
+    const int64_t count4 = m * L.pp / 4;
+    reduce_mod_kernel<<<grid_for(count4, sms), 256, 0, s>>>(reinterpret_cast<const int4*>(S), count4, t.m[l], t.rcpd[l],
+                                                            t.rcp[l], reinterpret_cast<uint32_t*>(R + (int64_t)l * m * L.pp));
+    if ((st = chk("residue reduction", 1)) != MM_OK) return st;
+  }
+  // Chinese remaindering, scaling and the binary64 store
+  switch (L.nmod) {
+    case 14: launch_combine<14>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+    case 15: launch_combine<15>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+    default: launch_combine<16>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+  }
+  return chk("CRT combine", 1);
 }
 
 }  // namespace mmb

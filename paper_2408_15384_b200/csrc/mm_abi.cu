@@ -668,12 +668,24 @@ int64_t product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
 }
 }  // namespace
 
+__attribute__((visibility("default"))) mm_status mm_f64_emu_plan(int64_t n, int* moduli, int* count, int* beta) {
+  if (n < 1 || !count || !beta) return MM_ERR_USAGE;
+  if (n > f64_emu_max_n()) return MM_ERR_UNSUPPORTED;
+  int mods[16];
+  const int c = f64_emu_moduli(n, beta, mods);
+  if (c == 0) return MM_ERR_UNSUPPORTED;
+  *count = c;
+  if (moduli)
+    for (int l = 0; l < c; ++l) moduli[l] = mods[l];
+  return MM_OK;
+}
+
 __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                                                                  mm_layout layout, int G) {
   if (m < 1 || n < 1 || p < 1 || G < 1) return 0;
-  if (dtype == MM_F64_EMU)  // plain products only: digit planes + INT32 partial + the INT8 product's own scratch
-    return (layout == MM_ROW_BLOCK && G == 1)
-               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, 8 * ((n + 15) / 16 * 16), p, MM_S8_S32)
+  if (dtype == MM_F64_EMU)  // plain products only: residue planes + INT32 product + the INT8 product's own scratch
+    return (layout == MM_ROW_BLOCK && G == 1 && n <= f64_emu_max_n())
+               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, n, p, MM_S8_S32)
                : 0;
   if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return 0;
   if (layout != MM_ROW_BLOCK && layout != MM_SUMMA_2D && layout != MM_SUMMA_25D) return 0;

@@ -138,3 +138,44 @@ def test_diag_knobs_refused_by_release_build(monkeypatch):
     out = subprocess.run(["strings", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "is a diagnostic knob of the diagnostic build only" in out
     assert "[mm trace]" not in out  # the timeline printers are compiled out of the release library
+
+
+def test_f64_emu_plan():
+    """mm_f64_emu_plan (MM_F64_EMU's host plan, csrc/f64_emu.cu) checked with exact integers: the
+    moduli are pairwise coprime and ≤ 256 (residues fit INT8), the scaled integer product fits the
+    symmetric CRT range (n·2^(2β) ≤ M/2 − 1, so Chinese remaindering recovers it exactly), β ≥ 53
+    (the binary64 width of every row / column maximum), β is the largest the product allows (≤ 60),
+    and no shorter prefix of the list would give β ≥ 53; INT32 sums bound n (n·2^14 < 2^31)."""
+    import math
+    lib = _lib.load()
+    mods, cnt, beta = (ctypes.c_int * 16)(), ctypes.c_int(), ctypes.c_int()
+    full = None
+    for n in (1, 2, 7, 8, 9, 100, 1000, 1500, 2049, 4096, 32768, 65536, 131071):
+        assert lib.mm_f64_emu_plan(n, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_OK, n
+        c, b = cnt.value, beta.value
+        ms = list(mods[:c])
+        if full is None or len(ms) > len(full):
+            full = ms
+        assert all(2 <= x <= 256 for x in ms)
+        assert all(math.gcd(x, y) == 1 for i, x in enumerate(ms) for y in ms[:i])
+        M = math.prod(ms)
+        assert n * 2 ** (2 * b) <= M // 2 - 1, (n, c, b)
+        assert b >= 53
+        assert b == 60 or n * 2 ** (2 * (b + 1)) > M // 2 - 1, (n, b)  # β maximal
+        Mless = math.prod(ms[:-1])
+        assert n * 2 ** (2 * 53) > Mless // 2 - 1, (n, c)  # the fewest moduli
+        assert n * (128 * 128) < 2 ** 31  # exact INT32 sums of residue products
+    # every plan uses a prefix of one fixed list
+    for n in (1, 1000, 131071):
+        assert lib.mm_f64_emu_plan(n, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_OK
+        assert list(mods[:cnt.value]) == full[:cnt.value]
+    assert lib.mm_f64_emu_plan(131072, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_ERR_UNSUPPORTED
+    assert lib.mm_f64_emu_plan(0, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_ERR_USAGE
+    assert lib.mm_f64_emu_plan(5, None, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_OK
+    assert lib.mm_f64_emu_plan(5, None, None, ctypes.byref(beta)) == _lib.MM_ERR_USAGE
+    # workspace: residue planes of A, B and C + the INT32 product (+ the INT8 product's own)
+    f = lib.mm_workspace_size
+    m, n, p = 2000, 1500, 1750
+    assert lib.mm_f64_emu_plan(n, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_OK
+    assert f(m, n, p, 3, 0, 1) >= cnt.value * (m * n + n * p + m * p) + 4 * m * p
+    assert f(m, 131072, p, 3, 0, 1) == 0 and f(m, n, p, 3, 0, 2) == 0

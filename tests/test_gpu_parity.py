@@ -789,10 +789,11 @@ def test_n_half_tail_same_bits_as_whole_tiles(mm, dt):
 
 @pytest.mark.parametrize("shape", [(256, 256, 256), (2000, 1500, 1750), (1000, 333, 517), (37, 4100, 29), (1, 1, 1)])
 def test_f64_emulation(mm, shape):
-    """MM_F64_EMU (f64_emu.cu): the binary64 product on the INT8 tensor cores via exact 7-bit digit
-    slices.  Exact-integer inputs (|x| <= 1024, K = 2049 pins) bit-exact — every digit product and
-    every scaled partial sum is exact; U[-1,1) inputs within the FP64 tolerance of the oracle and,
-    diagnostically, of DMMA's ~1e-16; ragged n (K padding) and p % 4 != 0 (byte digit stores)."""
+    """MM_F64_EMU (f64_emu.cu): the binary64 product on the INT8 tensor cores (integer scaling,
+    residues modulo 14-16 coprime moduli, one exact INT8 product per modulus, Chinese remaindering).
+    Exact-integer inputs (|x| <= 1024, K = 2049 pins) bit-exact — the scaling leaves integers
+    unrounded and the remaindering is exact; U[-1,1) inputs within the FP64 tolerance of the oracle
+    and, diagnostically, of DMMA's ~1e-16; ragged n (K padding) and p % 16 != 0 (padded planes)."""
     m, n, p = shape
     A, B = gen("f64", "exact", 71, m, n, p, 2049)
     Cref, _ = ref("f64", A, B)
@@ -808,6 +809,57 @@ def test_f64_emulation(mm, shape):
     assert err <= 1e-15, f"diagnostic: emulation error {err} well above DMMA's"
 
 
+def test_f64_emulation_dynamic_range(mm):
+    """MM_F64_EMU scales each row of A / column of B by its own power of two: rows spanning 2^-450 ..
+    2^450, columns 2^-450 .. 2^450 (products stay finite), one row decaying over 2^-60 inside itself, an all-zero row and
+    column, subnormal entries; the result matches the oracle within the FP64 tolerance (normalised by
+    Σ|a·b| per element) and within DMMA's ~1e-16 class diagnostically.  Zero rows / columns give
+    exact zeros."""
+    m, n, p = 300, 1000, 260
+    A, B = gen("f64", "random", 73, m, n, p)
+    rng = np.random.default_rng(73)
+    A = A * np.ldexp(1.0, rng.integers(-450, 450, m))[:, None]
+    B = B * np.ldexp(1.0, rng.integers(-450, 450, p))[None, :]
+    A[5] = A[5] * np.ldexp(1.0, -(np.arange(n) * 60 // n))  # within-row range of 2^60
+    A[7] = 0.0
+    B[:, 11] = 0.0
+    A[9] = np.ldexp(A[9], -1070)  # subnormal row (products underflow; the oracle's do too)
+    A[9, :3] = [4.9e-324, -4.9e-324, 0.0]
+    Cref, D = ref("f64", A, B)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    C = C.cpu().numpy()
+    assert np.all(C[7] == 0.0) and np.all(C[:, 11] == 0.0)
+    keep = np.ones(m, bool)
+    keep[9] = False  # subnormal row: compared in absolute terms below
+    err = oracle.normalized_error(C[keep], Cref[keep], D[keep])
+    assert err <= TOL["f64"], err
+    assert err <= 1e-15, f"diagnostic: emulation error {err} well above DMMA's"
+    assert np.max(np.abs(C[9] - Cref[9])) <= 1e-300
+
+
+def test_f64_emulation_long_k(mm):
+    """n beyond what 7-bit digit slicing allowed (33280): n = 70001 (ragged), exact-integer inputs
+    bit-exact against the oracle and random inputs within tolerance; n = 131072 (INT32 sums of
+    residue products could overflow) is refused with MM_ERR_UNSUPPORTED, not computed wrongly."""
+    m, n, p = 40, 70001, 36
+    A, B = gen("f64", "exact", 74, m, n, p, 2049)
+    Cref, _ = ref("f64", A, B)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    assert np.array_equal(C.cpu().numpy(), Cref)
+    A, B = gen("f64", "random", 75, m, n, p)
+    Cref, D = ref("f64", A, B)
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    err = oracle.normalized_error(C.cpu().numpy(), Cref, D)
+    assert err <= TOL["f64"] and err <= 1e-15, err
+    Ad = torch.zeros(2, 131072, dtype=torch.float64, device="cuda")
+    Bd = torch.zeros(131072, 2, dtype=torch.float64, device="cuda")
+    with pytest.raises(RuntimeError, match="131071|exact-INT32"):
+        mm.gemm(Ad, Bd, f64_emulation=True)
+
+
 def test_f64_emulation_config1_golden(mm):
     """C2x (configs[1] shape, K=2049 exact pin): the emulated product's full-output checksum equals
     SURVEY c7's golden, like DMMA's."""
@@ -819,8 +871,8 @@ def test_f64_emulation_config1_golden(mm):
 
 
 def test_config4_fp64_32768_emulated(mm):
-    """configs[4] at full size through MM_F64_EMU: the C5x exact pin (K=2049 integers; every digit
-    product, scaled partial and sum exact) hashes to the oracle's golden bit for bit; random U[-1,1)
+    """configs[4] at full size through MM_F64_EMU: the C5x exact pin (K=2049 integers; scaling,
+    residue products and remaindering exact) hashes to the oracle's golden bit for bit; random U[-1,1)
     inputs match the oracle on >= 64 seeded rows and >= 64 seeded columns (+ seams) within 1e-12,
     and diagnostically within 1e-15."""
     from synthgen import gpu as sgg
