@@ -46,8 +46,6 @@ struct CrtTab {
   int nmod;                       // N
   int beta;                       // β
   int m[kMaxMod];                 // m_l
-  float rcp[kMaxMod];             // 1/m_l (rounded; the reductions correct the quotient)
-  double rcpd[kMaxMod];           // 1/m_l in binary64
   // 0-based digits: C' = Σ_q v_q P_q with P_0 = 1, P_q = m[0] ... m[q-1]
   int pmod[kMaxMod][kMaxMod];     // pmod[q][k] = P_q mod m[k] for q < k
   int pinv[kMaxMod];              // (P_k mod m[k])^-1 mod m[k]
@@ -86,8 +84,6 @@ CrtTab make_tab(int nmod, int beta) {
   t.beta = beta;
   for (int l = 0; l < kMaxMod; ++l) {
     t.m[l] = kMods[l];
-    t.rcp[l] = 1.0f / (float)kMods[l];
-    t.rcpd[l] = 1.0 / (double)kMods[l];
   }
   for (int k = 0; k < kMaxMod; ++k) {
     int pk = 1 % kMods[k];  // P_0 mod m[k]
@@ -102,21 +98,60 @@ CrtTab make_tab(int nmod, int beta) {
 
 __device__ __forceinline__ int dec_exp(int v) { return v ? v - kExpBias : 0; }
 
-// x mod m in [0, m) for |x| < 2^24 (float quotient, corrected)
-__device__ __forceinline__ int mod_small(int x, int m, float rcp) {
-  const int q = __float2int_rd(__int2float_rn(x) * rcp);
-  int r = x - q * m;
-  r += r < 0 ? m : 0;
-  r -= r >= m ? m : 0;
-  return r;
+// 2^k for -1022 <= k <= 1023
+__device__ __forceinline__ double pow2(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
+
+// x·2^k, |k| ≤ 2044, in two exact steps of about k/2 (an element that underflows in the first step
+// is below 2^-590 of its row / column maximum and rounds to 0 anyway)
+__device__ __forceinline__ double scale2(double x, int k) {
+  const int a = k / 2;
+  return x * pow2(a) * pow2(k - a);
 }
 
-// symmetric residue in [-128, 127] of an integer-valued binary64 |x| < 2^62
-__device__ __forceinline__ int sym_residue(double x, int m, double rcpd, float rcp) {
-  const double q = floor(x * rcpd);
-  const int r0 = (int)fma(-q, (double)m, x);  // exact: |x - q m| < 8 m
-  int r = mod_small(r0, m, rcp);
-  return r > (m >> 1) - (m & 1 ? 0 : 1) ? r - m : r;  // odd m: [-(m-1)/2, (m-1)/2]; 256: [-128, 127]
+// x·2^k, |k| ≤ 3066, in three steps of about k/3: no intermediate underflows or overflows unless the
+// result does (|x| ≥ 1 or 0), so the result is x·2^k rounded once
+__device__ __forceinline__ double scale3(double x, int k) {
+  const int a = k / 3, b = (k - a) / 2;
+  return x * pow2(a) * pow2(b) * pow2(k - a - b);
+}
+
+
+// the moduli as compile-time constants once a loop over l is unrolled (x % m becomes a
+// multiply-high, not a division)
+__host__ __device__ constexpr int mod_at(int l) {
+  return l == 0 ? 256 : l == 1 ? 255 : l == 2 ? 253 : l == 3 ? 251 : l == 4 ? 247 : l == 5 ? 241 : l == 6 ? 239
+       : l == 7 ? 233 : l == 8 ? 229 : l == 9 ? 227 : l == 10 ? 223 : l == 11 ? 217 : l == 12 ? 211
+       : l == 13 ? 199 : l == 14 ? 197 : 193;
+}
+
+constexpr bool mod_at_matches() {
+  for (int l = 0; l < kMaxMod; ++l)
+    if (mod_at(l) != kMods[l]) return false;
+  return true;
+}
+static_assert(mod_at_matches(), "mod_at() and kMods[] list the same moduli");
+
+// x mod m in [0, m) for -2^30 < x < 2^30 (m a compile-time constant after unrolling)
+__device__ __forceinline__ int mod_of(int x, int m) {
+  const uint32_t bias = (uint32_t)m * ((1u << 30) / (uint32_t)m + 1u);  // multiple of m above 2^30
+  return (int)(((uint32_t)x + bias) % (uint32_t)m);
+}
+
+// symmetric residue (odd m: [-(m-1)/2, (m-1)/2]; 256: [-128, 127]) of an integer |a| ≤ 2^60 held as
+// limbs a = a2·2^40 + a1·2^20 + a0 (a0, a1 in [0, 2^20), a2 signed)
+__device__ __forceinline__ int sym_residue(int a2, int a1, int a0, int m) {
+  if (m == 256) return (int)(int8_t)(uint8_t)a0;  // low byte, two's complement
+  const int c20 = (int)((1u << 20) % (uint32_t)m), c40 = (int)(((uint64_t)1 << 40) % (uint64_t)m);
+  const int r = mod_of(a2 * c40 + a1 * c20 + a0, m);  // |·| < 2^29
+  return r > (m >> 1) ? r - m : r;
+}
+
+// x (|x| ≤ 2^60) rounded to the nearest integer (ties to even) as limbs
+__device__ __forceinline__ void limbs(double x, int& a2, int& a1, int& a0) {
+  const long long v = __double2ll_rn(x);
+  a0 = (int)(v & 0xFFFFF);
+  a1 = (int)((v >> 20) & 0xFFFFF);
+  a2 = (int)(v >> 40);
 }
 
 // e[i] = bias + frexp exponent of max_k |A[i][k]| (0 if the row is zero)
@@ -157,20 +192,20 @@ __global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_
 // A residue planes: Ar[(l*m + i)*kp + k] = a'_ik mod m_l (k >= n: 0); 4 consecutive k per thread
 template <int N>
 __global__ void residues_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t kp,
-                                  const int* __restrict__ e, int8_t* __restrict__ Ar, const __grid_constant__ CrtTab t) {
+                                  const int* __restrict__ e, int beta, int8_t* __restrict__ Ar) {
   const int64_t q4 = kp / 4;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * q4; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = w / q4, k0 = (w % q4) * 4;
-    const int sc = t.beta - dec_exp(e[i]);
-    double x[4];
+    const int sc = beta - dec_exp(e[i]);
+    const double s1 = pow2(sc / 2), s2 = pow2(sc - sc / 2);  // scale2, hoisted
+    int a2[4], a1[4], a0[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) x[c] = k0 + c < n ? rint(ldexp(A[i * lda + k0 + c], sc)) : 0.0;
+    for (int c = 0; c < 4; ++c) limbs(k0 + c < n ? A[i * lda + k0 + c] * s1 * s2 : 0.0, a2[c], a1[c], a0[c]);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       uint32_t word = 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        word |= (uint32_t)(uint8_t)(int8_t)sym_residue(x[c], t.m[l], t.rcpd[l], t.rcp[l]) << (8 * c);
+      for (int c = 0; c < 4; ++c) word |= (uint32_t)(uint8_t)(int8_t)sym_residue(a2[c], a1[c], a0[c], mod_at(l)) << (8 * c);
       *reinterpret_cast<uint32_t*>(Ar + ((int64_t)l * m + i) * kp + k0) = word;
     }
   }
@@ -179,45 +214,45 @@ __global__ void residues_a_kernel(const double* __restrict__ A, int64_t lda, int
 // B residue planes: Br[(l*n + k)*pp + j] = b'_kj mod m_l (j >= p: 0); 4 consecutive j per thread
 template <int N>
 __global__ void residues_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t p, int64_t pp,
-                                  const int* __restrict__ f, int8_t* __restrict__ Br, const __grid_constant__ CrtTab t) {
+                                  const int* __restrict__ f, int beta, int8_t* __restrict__ Br) {
   const int64_t q4 = pp / 4;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n * q4; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = w / q4, j0 = (w % q4) * 4;
-    double x[4];
+    int a2[4], a1[4], a0[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int64_t j = j0 + c;
-      x[c] = j < p ? rint(ldexp(B[k * ldb + j], t.beta - dec_exp(f[j]))) : 0.0;
+      limbs(j < p ? scale2(B[k * ldb + j], beta - dec_exp(f[j])) : 0.0, a2[c], a1[c], a0[c]);
     }
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       uint32_t word = 0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        word |= (uint32_t)(uint8_t)(int8_t)sym_residue(x[c], t.m[l], t.rcpd[l], t.rcp[l]) << (8 * c);
+      for (int c = 0; c < 4; ++c) word |= (uint32_t)(uint8_t)(int8_t)sym_residue(a2[c], a1[c], a0[c], mod_at(l)) << (8 * c);
       *reinterpret_cast<uint32_t*>(Br + ((int64_t)l * n + k) * pp + j0) = word;
     }
   }
 }
 
-// R[i*pp + j] = S[i*pp + j] mod m in [0, m) (S exact INT32 product of the residues), 4 per thread
-__global__ void reduce_mod_kernel(const int4* __restrict__ S, int64_t count4, int m, double rcpd, float rcp,
-                                  uint32_t* __restrict__ R) {
+// R[i*pp + j] = S[i*pp + j] mod m_L in [0, m_L) (S: the exact INT32 product of the residues), 4 per thread
+template <int L>
+__global__ void reduce_mod_kernel(const int4* __restrict__ S, int64_t count4, uint32_t* __restrict__ R) {
+  constexpr int m = mod_at(L);
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < count4; w += (int64_t)gridDim.x * blockDim.x) {
     const int4 v = S[w];
     const int s[4] = {v.x, v.y, v.z, v.w};
     uint32_t word = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const double q = floor((double)s[c] * rcpd);
-      const int r0 = (int)fma(-q, (double)m, (double)s[c]);  // exact, |r0| < 2m
-      word |= (uint32_t)mod_small(r0, m, rcp) << (8 * c);
+      // |s| < 2^31: split s = 2^16 h + lo, h signed, lo in [0, 2^16) (2^16 mod m is a constant)
+      const int h = s[c] >> 16, lo = s[c] & 0xFFFF;
+      word |= (uint32_t)mod_of(h * (int)((1u << 16) % (uint32_t)m) + lo, m) << (8 * c);
     }
     R[w] = word;
   }
 }
 
-// double-double t·m + v (m ≤ 256, |v| ≤ 128): Horner step of the mixed-radix value
+// double-double t·M + v (M < 2^24, |v| < 2^24): Horner step of the mixed-radix value
 __device__ __forceinline__ void dd_step(double& hi, double& lo, double m, double v) {
   const double p = hi * m;
   const double pe = fma(hi, m, -p);  // hi·m = p + pe exactly
@@ -229,38 +264,66 @@ __device__ __forceinline__ void dd_step(double& hi, double& lo, double m, double
   lo = l - (hi - s);
 }
 
-// C[i][j] (+)= 2^-(2β - e_i - f_j) · C'_ij, C' from its residues R_l by Garner + double-double Horner
+// C[i][j] (+)= 2^-(2β - e_i - f_j) · C'_ij, C' from its residues R_l by Garner + double-double Horner;
+// 4 consecutive j per thread (4-byte residue loads, the 4 elements' arithmetic interleaved), pp % 4 == 0
 template <int N>
-__global__ void crt_combine_kernel(const uint8_t* __restrict__ R, int64_t m, int64_t p, int64_t pp,
-                                   double* __restrict__ C, int64_t ldc, const int* __restrict__ e,
-                                   const int* __restrict__ f, int beta_one, const __grid_constant__ CrtTab t) {
-  const int64_t plane = m * pp;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * p; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = w / p, j = w % p;
-    const uint8_t* r = R + i * pp + j;
-    int v[N];
+__global__ void __launch_bounds__(256) crt_combine_kernel(const uint8_t* __restrict__ R, int64_t m, int64_t p,
+                                                          int64_t pp, double* __restrict__ C, int64_t ldc,
+                                                          const int* __restrict__ e, const int* __restrict__ f,
+                                                          int beta_one, const __grid_constant__ CrtTab t) {
+  constexpr int G = (N + 2) / 3;                  // digit triples (the last may be short)
+  constexpr int kTopBits = 8 * (N - 3 * (G - 1));  // bits of the top triple's value
+  constexpr int kPlain = (53 - kTopBits) / 24;    // Horner steps exact in binary64
+  const int64_t plane = m * pp, q4 = (p + 3) / 4;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * q4; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = w / q4, j0 = (w % q4) * 4;
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(R + i * pp + j0);
+    uint32_t word[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) word[k] = __ldg(r + k * (plane / 4));
+    // Garner: v_k = (c_k - Σ_{q<k} v_q (P_q mod m_k)) · (P_k mod m_k)^-1 mod m_k, symmetric digits
+    int v[4][N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      // v_k = (c_k - Σ_{j<k} v_j (P_j mod m_k)) · (P_k mod m_k)^-1 mod m_k, symmetric
-      int x = (int)__ldg(r + k * plane);
+      const int mk = mod_at(k);
 #pragma unroll
-      for (int q = 0; q < k; ++q) x -= v[q] * t.pmod[q][k];
-      const int y = mod_small(x, t.m[k], t.rcp[k]) * t.pinv[k];
-      const int d = mod_small(y, t.m[k], t.rcp[k]);
-      v[k] = d > (t.m[k] >> 1) ? d - t.m[k] : d;  // 256: [-127, 128]; odd: [-(m-1)/2, (m-1)/2]
-    }
-    // C' = v_0 + m_0 (v_1 + m_1 (v_2 + ...)): exact in binary64 while below 2^53 (the top 6
-    // digits: |value| < 2^48), double-double below
-    double hi = (double)v[N - 1], lo = 0.0;
+      for (int c = 0; c < 4; ++c) {
+        int x = (int)((word[k] >> (8 * c)) & 0xFF);
 #pragma unroll
-    for (int k = N - 2; k >= 0; --k) {
-      if (k >= N - 6) hi = fma(hi, (double)t.m[k], (double)v[k]);
-      else dd_step(hi, lo, (double)t.m[k], (double)v[k]);
+        for (int q = 0; q < k; ++q) x -= v[c][q] * t.pmod[q][k];  // |x| < 2^19
+        const int d = mod_of(mod_of(x, mk) * t.pinv[k], mk);
+        v[c][k] = d > (mk >> 1) ? d - mk : d;  // 256: [-127, 128]; odd: [-(m-1)/2, (m-1)/2]
+      }
     }
-    const int ei = e[i], fj = f[j];
-    const double val = (ei && fj) ? ldexp(hi + lo, dec_exp(ei) + dec_exp(fj) - 2 * t.beta) : 0.0;
-    double* c = C + i * ldc + j;
-    *c = beta_one ? *c + val : val;
+    const int ei = e[i];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // triples w_g = v_3g + m_3g (v_3g+1 + m_3g+1 v_3g+2) (|w| < 2^24, exact) in radix M_g = m_3g m_3g+1 m_3g+2:
+      // C' = w_0 + M_0 (w_1 + M_1 (w_2 + ...)), Horner exact while below 2^53, double-double below
+      int wg[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        int acc = 0;
+#pragma unroll
+        for (int k = 3 * g + 2; k >= 3 * g; --k)
+          if (k < N) acc = acc * mod_at(k) + v[c][k];
+        wg[g] = acc;
+      }
+      double hi = (double)wg[G - 1], lo = 0.0;
+#pragma unroll
+      for (int g = G - 2; g >= 0; --g) {
+        const double M = (double)(mod_at(3 * g) * mod_at(3 * g + 1) * mod_at(3 * g + 2));
+        if (g >= G - 1 - kPlain) hi = fma(hi, M, (double)wg[g]);
+        else dd_step(hi, lo, M, (double)wg[g]);
+      }
+      const int64_t j = j0 + c;
+      if (j < p) {
+        const int fj = f[j];
+        const double val = (ei && fj) ? scale3(hi + lo, dec_exp(ei) + dec_exp(fj) - 2 * t.beta) : 0.0;
+        double* cp = C + i * ldc + j;
+        *cp = beta_one ? *cp + val : val;
+      }
+    }
   }
 }
 
@@ -295,14 +358,28 @@ template <int N>
 void launch_residues(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n, int64_t p,
                      const Layout& L, const int* e, const int* f, int8_t* Ar, int8_t* Br, const CrtTab& t, int sms,
                      cudaStream_t s) {
-  residues_a_kernel<N><<<grid_for(m * (L.kp / 4), sms), 256, 0, s>>>(A, lda, m, n, L.kp, e, Ar, t);
-  residues_b_kernel<N><<<grid_for(n * (L.pp / 4), sms), 256, 0, s>>>(B, ldb, n, p, L.pp, f, Br, t);
+  residues_a_kernel<N><<<grid_for(m * (L.kp / 4), sms), 256, 0, s>>>(A, lda, m, n, L.kp, e, t.beta, Ar);
+  residues_b_kernel<N><<<grid_for(n * (L.pp / 4), sms), 256, 0, s>>>(B, ldb, n, p, L.pp, f, t.beta, Br);
 }
 
 template <int N>
 void launch_combine(const uint8_t* R, int64_t m, int64_t p, int64_t pp, double* C, int64_t ldc, const int* e,
                     const int* f, int beta_one, const CrtTab& t, int sms, cudaStream_t s) {
-  crt_combine_kernel<N><<<grid_for(m * p, sms), 256, 0, s>>>(R, m, p, pp, C, ldc, e, f, beta_one, t);
+  crt_combine_kernel<N><<<grid_for(m * ((p + 3) / 4), sms), 256, 0, s>>>(R, m, p, pp, C, ldc, e, f, beta_one, t);
+}
+
+template <int L>
+void reduce_at(const int4* S, int64_t count4, uint32_t* R, int sms, cudaStream_t s) {
+  reduce_mod_kernel<L><<<grid_for(count4, sms), 256, 0, s>>>(S, count4, R);
+}
+
+void launch_reduce(int l, const int4* S, int64_t count4, uint32_t* R, int sms, cudaStream_t s) {
+  using Fn = void (*)(const int4*, int64_t, uint32_t*, int, cudaStream_t);
+  static constexpr Fn fns[kMaxMod] = {reduce_at<0>,  reduce_at<1>,  reduce_at<2>,  reduce_at<3>,
+                                      reduce_at<4>,  reduce_at<5>,  reduce_at<6>,  reduce_at<7>,
+                                      reduce_at<8>,  reduce_at<9>,  reduce_at<10>, reduce_at<11>,
+                                      reduce_at<12>, reduce_at<13>, reduce_at<14>, reduce_at<15>};
+  fns[l](S, count4, R, sms, s);
 }
 
 }  // namespace
@@ -368,9 +445,8 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp, S, L.pp,
                  0, s);
     if (st != MM_OK) return st;
-    const int64_t count4 = m * L.pp / 4;
-    reduce_mod_kernel<<<grid_for(count4, sms), 256, 0, s>>>(reinterpret_cast<const int4*>(S), count4, t.m[l], t.rcpd[l],
-                                                            t.rcp[l], reinterpret_cast<uint32_t*>(R + (int64_t)l * m * L.pp));
+    launch_reduce(l, reinterpret_cast<const int4*>(S), m * L.pp / 4, reinterpret_cast<uint32_t*>(R + (int64_t)l * m * L.pp),
+                  sms, s);
     if ((st = chk("residue reduction", 1)) != MM_OK) return st;
   }
   // Chinese remaindering, scaling and the binary64 store

@@ -834,7 +834,14 @@ def test_f64_emulation_dynamic_range(mm):
     keep[9] = False  # subnormal row: compared in absolute terms below
     err = oracle.normalized_error(C[keep], Cref[keep], D[keep])
     assert err <= TOL["f64"], err
+    keep[5] = False
+    err = oracle.normalized_error(C[keep], Cref[keep], D[keep])
     assert err <= 1e-15, f"diagnostic: emulation error {err} well above DMMA's"
+    # row 5 (its elements fall to 2^-60 of its maximum): each a_5k carries a scaling error up to
+    # 2^-54 of the row maximum, while D counts |a_5k| itself — the a-priori bound is
+    # 2^-53 · max|a_5·| · Σ|b| / D ≈ 2^-53 · 60/ln 2 / 2 ≈ 5e-15 of D
+    err5 = oracle.normalized_error(C[5], Cref[5], D[5])
+    assert err5 <= 1e-14, err5
     assert np.max(np.abs(C[9] - Cref[9])) <= 1e-300
 
 
