@@ -25,8 +25,8 @@
  *                                               inputs; finite inputs only; n < 131072 (n·2^14 <
  *                                               2^31 per INT32 sum); device scratch ≈
  *                                               N·(m·n + n·p + m·p) + 4·m·p bytes
- *                                               (mm_workspace_size); plain products only, not for
- *                                               mm_gemm_sharded)
+ *                                               (mm_workspace_size); every layout of
+ *                                               mm_gemm_sharded, its local products emulated)
  *   MM_S8_S32   int8     × int8     → int32    (INT32 accumulate, exact while
  *                                               n·128² < 2^31; BASELINE.json config 2)
  *
@@ -141,7 +141,7 @@ const char* mm_last_error(const mm_ctx* ctx);
  *   only layer 0's are valid and are broadcast along the depth first); layer l
  *   runs the SUMMA k-panels t ≡ l (mod c), and the layers' C blocks are summed
  *   onto layer 0 (NCCL reduce); other layers' C_local hold partial sums.
- *   SUMMA layouts are implemented for MM_F64 (they accumulate with β = 1).
+ *   SUMMA layouts are implemented for MM_F64 and MM_F64_EMU (they accumulate with β = 1).
  *
  * Mismatched arguments across ranks are a usage error: the diagnostic build (and the release
  * library with MM_CHECK_COLLECTIVE=1, at the cost of one all-reduce and a stream synchronisation)
@@ -256,7 +256,7 @@ typedef struct {
  * 0 = the library default.  Writes at most `cap` steps to `steps` (may be NULL with cap 0) and the
  * plan's metadata to *info (required).  Returns MM_ERR_USAGE for invalid arguments (the same checks
  * as mm_gemm_sharded: dims >= 1, 0 <= r < G, root in range, grid consistent with G, flags valid for
- * the layout; SUMMA layouts for MM_F64 only).  Pure host logic. */
+ * the layout; SUMMA layouts for MM_F64 and MM_F64_EMU only).  Pure host logic. */
 mm_status mm_shard_plan(int64_t m, int64_t n, int64_t p, mm_dtype dtype, mm_layout layout, int grid_rows,
                         int grid_cols, unsigned flags, int root, int G, int r, int64_t panel,
                         mm_plan_step* steps, int cap, mm_plan_info* info);

@@ -180,15 +180,23 @@ def summa_panels(n: int, grid_rows: int, grid_cols: int, panel: int):
     return [(k0[i], kw[i], ao[i], bo[i]) for i in range(cnt)]
 
 
+def _dtype_code(dtype: torch.dtype, f64_emulation: bool) -> int:
+    if f64_emulation:
+        if dtype != torch.float64:
+            raise ValueError("f64_emulation needs float64 operands")
+        return MM_F64_EMU
+    return IN_DTYPE[dtype]
+
+
 def shard_plan(m: int, n: int, p: int, dtype: torch.dtype, *, layout: int = MM_ROW_BLOCK,
                grid: tuple[int, int] = (0, 0), flags: int = 0, root: int = 0, world: int = 1, rank: int = 0,
-               panel: int = 0):
+               panel: int = 0, f64_emulation: bool = False):
     """The plan rank `rank` of `world` runs for mm_gemm_sharded (include/mm.h, mm_shard_plan):
     (steps, info) with steps a list of dicts (op/buffer/communicator names resolved) and info a dict
     with the communicator split colours/keys and the staging-buffer sizes."""
     lib = _lib.load()
     info = _lib.PlanInfo()
-    dt = IN_DTYPE[dtype]
+    dt = _dtype_code(dtype, f64_emulation)
     st = lib.mm_shard_plan(m, n, p, dt, layout, grid[0], grid[1], flags, root, world, rank, panel, None, 0,
                            ctypes.byref(info))
     if st != 0:
@@ -211,9 +219,10 @@ def shard_plan(m: int, n: int, p: int, dtype: torch.dtype, *, layout: int = MM_R
     return steps, meta
 
 
-def workspace_size(m: int, n: int, p: int, dtype: torch.dtype, layout: int = MM_ROW_BLOCK, world: int = 1) -> int:
+def workspace_size(m: int, n: int, p: int, dtype: torch.dtype, layout: int = MM_ROW_BLOCK, world: int = 1,
+                   f64_emulation: bool = False) -> int:
     """Upper bound of the device scratch a context allocates for such a call (mm_workspace_size)."""
-    return int(_lib.load().mm_workspace_size(m, n, p, IN_DTYPE[dtype], layout, world))
+    return int(_lib.load().mm_workspace_size(m, n, p, _dtype_code(dtype, f64_emulation), layout, world))
 
 
 def ipc_export(t: torch.Tensor) -> bytes:
@@ -293,9 +302,11 @@ def _nccl_comm_ptr(group) -> int:
 def gemm_sharded(m: int, n: int, p: int, dtype: torch.dtype, A_local: torch.Tensor | None,
                  B_local: torch.Tensor, C_local: torch.Tensor | None, *, layout: int = MM_ROW_BLOCK,
                  grid: tuple[int, int] = (0, 0), flags: int = 0, root: int = 0,
-                 C_full: torch.Tensor | None = None, group=None, stream: torch.cuda.Stream | None = None):
-    """Collective product over an NCCL process group (see include/mm.h, mm_gemm_sharded)."""
-    dt = IN_DTYPE[dtype]
+                 C_full: torch.Tensor | None = None, group=None, stream: torch.cuda.Stream | None = None,
+                 f64_emulation: bool = False):
+    """Collective product over an NCCL process group (see include/mm.h, mm_gemm_sharded);
+    f64_emulation (float64): every local product as MM_F64_EMU."""
+    dt = _dtype_code(dtype, f64_emulation)
     dev = B_local.device
     ctx = context(dev.index)
     s = stream if stream is not None else torch.cuda.current_stream(dev)

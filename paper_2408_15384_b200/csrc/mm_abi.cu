@@ -666,6 +666,11 @@ int64_t product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
   }
   return pad + round_up(slabs, 256) + round_up(std::max<int64_t>(flags, 256), 256);
 }
+// MM_F64_EMU: residue planes + INT32 product + the INT8 product's own scratch
+int64_t emu_or_product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
+  if (dt != MM_F64_EMU) return product_scratch(m, n, p, dt);
+  return (int64_t)f64_emu_scratch(m, n, p) + product_scratch(m, n, p, MM_S8_S32);
+}
 }  // namespace
 
 __attribute__((visibility("default"))) mm_status mm_f64_emu_plan(int64_t n, int* moduli, int* count, int* beta) {
@@ -683,13 +688,10 @@ __attribute__((visibility("default"))) mm_status mm_f64_emu_plan(int64_t n, int*
 __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64_t n, int64_t p, mm_dtype dtype,
                                                                  mm_layout layout, int G) {
   if (m < 1 || n < 1 || p < 1 || G < 1) return 0;
-  if (dtype == MM_F64_EMU)  // plain products only: residue planes + INT32 product + the INT8 product's own scratch
-    return (layout == MM_ROW_BLOCK && G == 1 && n <= f64_emu_max_n())
-               ? f64_emu_scratch(m, n, p) + (size_t)product_scratch(m, n, p, MM_S8_S32)
-               : 0;
-  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return 0;
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32 && dtype != MM_F64_EMU) return 0;
+  if (dtype == MM_F64_EMU && n > f64_emu_max_n()) return 0;
   if (layout != MM_ROW_BLOCK && layout != MM_SUMMA_2D && layout != MM_SUMMA_25D) return 0;
-  if (layout != MM_ROW_BLOCK && dtype != MM_F64) return 0;
+  if (layout != MM_ROW_BLOCK && dtype != MM_F64 && dtype != MM_F64_EMU) return 0;
   knobs_refresh();
   int64_t best = 0;
   auto consider = [&](int pr, int pc, unsigned flags) {
@@ -703,12 +705,12 @@ __attribute__((visibility("default"))) size_t mm_workspace_size(int64_t m, int64
       for (int i = 0; i < 4; ++i) total += round_up(std::max<int64_t>(info.stage_bytes[i], 0), 256);
       int64_t g = 0;
       for (const mm_plan_step& s : steps)
-        if (s.op == MM_OP_GEMM) g = std::max(g, product_scratch(s.m, s.n, s.p, dtype));
+        if (s.op == MM_OP_GEMM) g = std::max(g, emu_or_product_scratch(s.m, s.n, s.p, dtype));
       best = std::max(best, total + g);
       if (G == 1) break;
     }
   };
-  if (G == 1 && layout == MM_ROW_BLOCK) return (size_t)product_scratch(m, n, p, dtype);
+  if (G == 1 && layout == MM_ROW_BLOCK) return (size_t)emu_or_product_scratch(m, n, p, dtype);
   if (layout == MM_ROW_BLOCK) {
     consider(0, 0, MM_BCAST_B);  // staging buffers of the broadcast (the largest variant)
     consider(0, 0, 0);

@@ -35,8 +35,8 @@ Range shard(int64_t total, int G, int r) {
   mm_shard_range(total, G, r, &x.start, &x.count);
   return x;
 }
-int64_t esz_in(mm_dtype t) { return t == MM_F64 ? 8 : (t == MM_BF16_F32 ? 2 : 1); }
-int64_t esz_out(mm_dtype t) { return t == MM_F64 ? 8 : 4; }
+int64_t esz_in(mm_dtype t) { return (t == MM_F64 || t == MM_F64_EMU) ? 8 : (t == MM_BF16_F32 ? 2 : 1); }
+int64_t esz_out(mm_dtype t) { return (t == MM_F64 || t == MM_F64_EMU) ? 8 : 4; }
 
 // event ids
 enum { EV_START = 0, EV_END = 1, EV_READY0 = 2, EV_FREE0 = 4, EV_COUNT = 6 };
@@ -271,7 +271,7 @@ __attribute__((visibility("default"))) mm_status mm_shard_plan(int64_t m, int64_
   for (int c = 0; c < 4; ++c) info->color[c] = info->key[c] = -1;
   info->color[MM_COMM_WORLD] = 0;
   info->key[MM_COMM_WORLD] = r;
-  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32) return MM_ERR_USAGE;
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32 && dtype != MM_F64_EMU) return MM_ERR_USAGE;
   if (m < 1 || n < 1 || p < 1 || G < 1 || r < 0 || r >= G || cap < 0 || (cap > 0 && !steps)) return MM_ERR_USAGE;
   Builder b;
   if (layout == MM_ROW_BLOCK) {
@@ -281,7 +281,8 @@ __attribute__((visibility("default"))) mm_status mm_shard_plan(int64_t m, int64_
     if ((flags & MM_C_WINDOW) && !(flags & MM_GATHER_C_FUSED)) return MM_ERR_USAGE;  // (executor detail only)
     row_block(b, info, m, n, p, dtype, flags, root, G, r, panel);
   } else if (layout == MM_SUMMA_2D || layout == MM_SUMMA_25D) {
-    if (dtype != MM_F64) return MM_ERR_UNSUPPORTED;  // panels accumulate with beta = 1 (FP64 kernel)
+    // panels accumulate with beta = 1 (the FP64 kernel and the FP64 emulation's reconstruction)
+    if (dtype != MM_F64 && dtype != MM_F64_EMU) return MM_ERR_UNSUPPORTED;
     if (grid_rows < 1 || grid_cols < 1) return MM_ERR_USAGE;
     const int g2 = grid_rows * grid_cols;
     if (layout == MM_SUMMA_2D && (g2 != G || flags)) return MM_ERR_USAGE;

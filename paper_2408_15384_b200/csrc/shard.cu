@@ -436,7 +436,7 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
   if (!ctx) return MM_ERR_USAGE;
   knobs_refresh();
   DeviceGuard dg(ctx->device);
-  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32)
+  if (dtype != MM_F64 && dtype != MM_BF16_F32 && dtype != MM_S8_S32 && dtype != MM_F64_EMU)
     return set_err(ctx, MM_ERR_USAGE, "unknown dtype %d", (int)dtype);
   if (m < 1 || n < 1 || p < 1) return set_err(ctx, MM_ERR_USAGE, "dimensions must be >= 1");
   if (!nccl_comm) return set_err(ctx, MM_ERR_USAGE, "nccl_comm is NULL");
@@ -491,8 +491,8 @@ __attribute__((visibility("default"))) mm_status mm_gemm_sharded(mm_ctx* ctx, in
     if ((flags & (MM_GATHER_C | MM_GATHER_C_FUSED)) && r == root && !C_full)
       return set_err(ctx, MM_ERR_USAGE, "MM_GATHER_C / MM_GATHER_C_FUSED need C_full on the root rank");
   } else if (layout == MM_SUMMA_2D || layout == MM_SUMMA_25D) {
-    if (dtype != MM_F64)
-      return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_SUMMA_2D/25D accumulate across k-panels; implemented for MM_F64");
+    if (dtype != MM_F64 && dtype != MM_F64_EMU)
+      return set_err(ctx, MM_ERR_UNSUPPORTED, "MM_SUMMA_2D/25D accumulate across k-panels; implemented for MM_F64 and MM_F64_EMU");
     if (layout == MM_SUMMA_2D && (grid_rows < 1 || grid_cols < 1 || grid_rows * grid_cols != G))
       return set_err(ctx, MM_ERR_USAGE, "grid %d x %d does not match communicator size %d", grid_rows, grid_cols, G);
     if (layout == MM_SUMMA_2D && flags)

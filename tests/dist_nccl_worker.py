@@ -151,7 +151,10 @@ def summa_small(G, r, checks):
     for layers in (2, 4, 8):
         if G % layers == 0 and layers > 1:
             cases += [(mm.MM_SUMMA_25D, g, mm.MM_REPLICATE) for g in grids_of(G // layers)]
-    for layout, (pr, pc), flags in cases:
+    # the same layouts with every local product emulated on the INT8 tensor cores (MM_F64_EMU)
+    cases += [(layout, g, flags, True) for layout, g, flags in cases[:2]]
+    for layout, (pr, pc), flags, *emu in cases:
+        emu = bool(emu)
         g2 = pr * pc
         l, r2 = r // g2, r % g2
         gi, gj = r2 // pc, r2 % pc
@@ -165,7 +168,7 @@ def summa_small(G, r, checks):
         os.environ["MM_SUMMA_PANEL"] = "128"
         try:
             mm.gemm_sharded(m, n, p, torch.float64, to_dev(Ab, "f64"), to_dev(Bb, "f64"), Cb, layout=layout,
-                            grid=(pr, pc), flags=flags)
+                            grid=(pr, pc), flags=flags, f64_emulation=emu)
         finally:
             os.environ.pop("MM_SUMMA_PANEL", None)
         mm.sync_check()
@@ -173,7 +176,8 @@ def summa_small(G, r, checks):
         ok = True
         if l == 0:
             ok = np.array_equal(Cb.cpu().numpy(), Cref[am[0]:am[0] + am[1], bn[0]:bn[0] + bn[1]])
-        checks.append({"what": f"{'SUMMA' if layout == mm.MM_SUMMA_2D else '2.5D'} {pr}x{pc}x{G // g2} f64 "
+        checks.append({"what": f"{'SUMMA' if layout == mm.MM_SUMMA_2D else '2.5D'} {pr}x{pc}x{G // g2} "
+                               f"{'f64 emulated' if emu else 'f64'} "
                                f"{m}x{n}x{p}", "ok": allreduce_ok(ok)})
 
 

@@ -178,4 +178,4 @@ def test_f64_emu_plan():
     m, n, p = 2000, 1500, 1750
     assert lib.mm_f64_emu_plan(n, mods, ctypes.byref(cnt), ctypes.byref(beta)) == _lib.MM_OK
     assert f(m, n, p, 3, 0, 1) >= cnt.value * (m * n + n * p + m * p) + 4 * m * p
-    assert f(m, 131072, p, 3, 0, 1) == 0 and f(m, n, p, 3, 0, 2) == 0
+    assert f(m, 131072, p, 3, 0, 1) == 0 and f(m, n, p, 3, 0, 2) >= f(m, n, p, 3, 0, 1) // 2  # sharded: local products

@@ -160,6 +160,27 @@ def test_workspace_size_bounds_allocation(mm):
         assert torch.equal(out.to(torch.float64), _exact_ref(tA, tB))
 
 
+def test_workspace_size_bounds_allocation_f64_emulated(mm):
+    """The same bound for MM_F64_EMU: residue planes, INT32 product and the INT8 product's scratch."""
+    m, n, p = 2000, 1500, 1750
+    g = torch.Generator(device="cuda").manual_seed(92)
+    A = torch.randint(-1000, 1000, (m, n), generator=g, device="cuda").double()
+    B = torch.randint(-1000, 1000, (n, p), generator=g, device="cuda").double()
+    torch.cuda.synchronize()
+    ctx = mm.Context(0)
+    out = torch.empty(m, p, dtype=torch.float64, device="cuda")
+    free1 = torch.cuda.mem_get_info()[0]
+    from paper_2408_15384_b200 import _lib
+    s = torch.cuda.current_stream().cuda_stream
+    ctx.check(_lib.load().mm_gemm(ctx.handle, m, n, p, mm.MM_F64_EMU, A.data_ptr(), B.data_ptr(), out.data_ptr(), s))
+    ctx.check(_lib.load().mm_sync_check(ctx.handle, s))
+    used = free1 - torch.cuda.mem_get_info()[0]
+    bound = mm.workspace_size(m, n, p, torch.float64, f64_emulation=True)
+    ctx.close()
+    assert used <= bound + (8 << 20), (used, bound)
+    assert torch.equal(out, A @ B)  # exact integers: cuBLAS's DGEMM is exact here too
+
+
 def test_clock_meter(mm):
     """mm_clock_meter: records the effective SM clock of a product kernel without changing it."""
     for dt, m, n, p in [("bf16", 4096, 4096, 4096), ("f64", 1024, 1024, 1024), ("i8", 2048, 2048, 2048)]:

@@ -118,6 +118,36 @@ def test_summa_world1_fp64(pg, panel):
         os.environ.pop("MM_SUMMA_PANEL", None)
 
 
+@pytest.mark.parametrize("layout", ["summa", "row_block"])
+def test_sharded_world1_fp64_emulated(pg, layout):
+    """MM_F64_EMU through mm_gemm_sharded (real NCCL calls at world size 1): SUMMA k-panels of 256
+    accumulate into C (β = 1: each panel's emulated product is rounded once, then added) and the
+    row block with B broadcast + gather; exact-integer inputs bit-exact, random inputs within the
+    FP64 tolerance and the DMMA-class diagnostic."""
+    import paper_2408_15384_b200 as mm
+    m, n, p = 700, 1000, 900
+    kw = dict(layout=mm.MM_SUMMA_2D, grid=(1, 1)) if layout == "summa" else \
+        dict(flags=mm.MM_BCAST_B | mm.MM_GATHER_C)
+    os.environ["MM_SUMMA_PANEL"] = "256"
+    try:
+        for kind in ("exact", "random"):
+            A, B = (sg.exact_f64(36, 1, 2049, m, n), sg.exact_f64(36, 2, 2049, n, p)) if kind == "exact" else \
+                (sg.uniform_f64(37, 1, m, n), sg.uniform_f64(37, 2, n, p))
+            C = torch.empty(m, p, dtype=torch.float64, device="cuda")
+            Cf = torch.empty(m, p, dtype=torch.float64, device="cuda") if layout == "row_block" else None
+            mm.gemm_sharded(m, n, p, torch.float64, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), C,
+                            C_full=Cf, f64_emulation=True, **kw)
+            mm.sync_check()
+            got = (Cf if Cf is not None else C).cpu().numpy()
+            if kind == "exact":
+                assert np.array_equal(got, oracle.gemm_f64(A, B))
+            else:
+                err = oracle.normalized_error(got, oracle.gemm_f64(A, B), oracle.absden_f64(A, B))
+                assert err <= 1e-12 and err <= 1e-15, err
+    finally:
+        os.environ.pop("MM_SUMMA_PANEL", None)
+
+
 def test_sharded_usage_errors(pg):
     import paper_2408_15384_b200 as mm
     t = torch.zeros(4, 4, dtype=torch.float64, device="cuda")

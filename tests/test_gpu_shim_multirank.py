@@ -25,14 +25,14 @@ import synthgen as sg
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 FAKE = os.path.join(ROOT, "tests", "libfakenccl.so")
-DT_CODE = {"f64": 0, "bf16": 1, "i8": 2}
-TIN = {"f64": torch.float64, "bf16": torch.bfloat16, "i8": torch.int8}
-TOUT = {"f64": torch.float64, "bf16": torch.float32, "i8": torch.int32}
-KEXACT = {"f64": 2049, "bf16": 9, "i8": 255}
+DT_CODE = {"f64": 0, "bf16": 1, "i8": 2, "emu": 3}  # emu: MM_F64_EMU (float64 operands)
+TIN = {"f64": torch.float64, "bf16": torch.bfloat16, "i8": torch.int8, "emu": torch.float64}
+TOUT = {"f64": torch.float64, "bf16": torch.float32, "i8": torch.int32, "emu": torch.float64}
+KEXACT = {"f64": 2049, "bf16": 9, "i8": 255, "emu": 2049}
 
 
 def _inputs(kind, m, n, p, seed=77):
-    gen = {"f64": sg.exact_f64, "bf16": sg.exact_bf16, "i8": sg.exact_i8}[kind]
+    gen = {"f64": sg.exact_f64, "bf16": sg.exact_bf16, "i8": sg.exact_i8, "emu": sg.exact_f64}[kind]
     return gen(seed, 1, KEXACT[kind], m, n), gen(seed, 2, KEXACT[kind], n, p)
 
 
@@ -144,7 +144,7 @@ def _check(world, cases, out):
                 assert out[(i, r)]["status"] == 2 and "differ across" in out[(i, r)]["error"], out[(i, r)]
             continue
         A, B = _inputs(kind, m, n, p)
-        Cref = px._local_product(kind, A, B).astype(np.float64)
+        Cref = px._local_product("f64" if kind == "emu" else kind, A, B).astype(np.float64)
         if layout == mm.MM_ROW_BLOCK:
             if flags & (mm.MM_GATHER_C | mm.MM_GATHER_C_FUSED):
                 assert np.array_equal(out[(i, root)]["CFULL"].astype(np.float64), Cref), case_name(cases[i])
@@ -187,6 +187,9 @@ def test_row_block_real_executor(mmod, world):
         kind = ("bf16", "i8", "f64")[j % 3]
         cases.append((mm.MM_ROW_BLOCK, kind, 600 + 37 * world, 512, 776, flags, (j + 1) % world, (0, 0),
                       "1" if j == 0 else None))
+    # the emulated FP64 product through the same executor (B broadcast + fused gather)
+    cases.append((mm.MM_ROW_BLOCK, "emu", 520 + 11 * world, 700, 333, mm.MM_BCAST_B | mm.MM_GATHER_C_FUSED,
+                  world - 1, (0, 0), None))
     cases.append((mm.MM_ROW_BLOCK, "f64", 64, 32, 48, 0, 0, (0, 0), "mismatch"))
     _check(world, cases, _run(world, cases))
 
@@ -195,9 +198,11 @@ def test_row_block_real_executor(mmod, world):
 def test_summa_real_executor(mmod, world, grids):
     mm = mmod
     cases = [(mm.MM_SUMMA_2D, "f64", 331, 357 + 16 * world, 313, 0, 0, g, None) for g in grids]
+    cases.append((mm.MM_SUMMA_2D, "emu", 301, 389, 277, 0, 0, grids[0], None))  # k-panels accumulate (β = 1)
     if world == 4:
         cases.append((mm.MM_SUMMA_25D, "f64", 297, 450, 283, mm.MM_REPLICATE, 0, (1, 2), None))
         cases.append((mm.MM_SUMMA_25D, "f64", 297, 450, 283, mm.MM_REPLICATE, 0, (2, 1), None))
+        cases.append((mm.MM_SUMMA_25D, "emu", 297, 450, 283, mm.MM_REPLICATE, 0, (1, 2), None))
     if world == 2:
         cases.append((mm.MM_SUMMA_25D, "f64", 297, 450, 283, mm.MM_REPLICATE, 0, (1, 1), None))
     _check(world, cases, _run(world, cases))
