@@ -74,20 +74,23 @@ struct Builder {
 };
 
 // Default column-panel width of the B broadcast: p/8, a 16-element multiple (every panel pitch
-// 16-B aligned for TMA).
-int64_t bcast_panel(int64_t p, int64_t panel) {
+// 16-B aligned for TMA).  MM_F64_EMU: p/2 — each panel is a separate emulated product whose
+// fixed costs (the residues of the whole local A, the reconstruction) do not shrink with its width.
+int64_t bcast_panel(int64_t p, int64_t panel, mm_dtype dt) {
   int64_t w = panel;
   if (w <= 0) {
-    int64_t npan = 8;
+    int64_t npan = dt == MM_F64_EMU ? 2 : 8;
     if (const char* e = mmb::knob("MM_BCAST_PANELS")) npan = std::max<int64_t>(1, atoll(e));  // tuning knob
     w = (p + npan - 1) / npan;
   }
   w = (w + 15) / 16 * 16;
   return std::min(w, p);
 }
-int64_t summa_panel(int64_t panel) {
+// Default k-panel width of SUMMA: 2048; MM_F64_EMU: 8192 (every panel's emulated product
+// reconstructs the whole local C block, so fewer, wider panels)
+int64_t summa_panel(int64_t panel, mm_dtype dt) {
   if (panel > 0) return panel;
-  int64_t w = 2048;
+  int64_t w = dt == MM_F64_EMU ? 8192 : 2048;
   if (const char* e = mmb::knob("MM_SUMMA_PANEL")) w = std::max<int64_t>(16, atoll(e));  // tuning knob
   return w;
 }
@@ -105,7 +108,7 @@ void row_block(Builder& b, mm_plan_info* info, int64_t m, int64_t n, int64_t p, 
     toff = mine.start * p * eo;
   }
   if (flags & MM_BCAST_B) {
-    const int64_t w = bcast_panel(p, panel);
+    const int64_t w = bcast_panel(p, panel, dt);
     const int64_t J = (p + w - 1) / w;
     info->stage_bytes[0] = info->stage_bytes[1] = n * w * ei;
     b.record(EV_START, 0);
@@ -168,7 +171,7 @@ void summa(Builder& b, mm_plan_info* info, int64_t m, int64_t n, int64_t p, mm_d
     if (bk.count > 0 && bn.count > 0) b.coll(MM_OP_BCAST, 0, MM_COMM_DEPTH, 0, MM_BUF_B, 0, bk.count * bn.count * ei);
     b.add(MM_OP_GROUP_END);
   }
-  const int64_t w = summa_panel(panel);
+  const int64_t w = summa_panel(panel, dt);
   const int np = mm_summa_panels(n, pr, pc, w, 0, nullptr, nullptr, nullptr, nullptr);
   std::vector<int64_t> k0(np), kw(np);
   std::vector<int> ao(np), bo(np);

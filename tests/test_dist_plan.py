@@ -227,18 +227,23 @@ def test_plan_race_free_and_shapes():
 
 def test_emulated_fp64_plans_equal_fp64_plans():
     """MM_F64_EMU shards like MM_F64 (same element sizes, same β = 1 panel accumulation): for every
-    layout, rank and flag set the plans are step-for-step identical, so the gloo executions of the
-    FP64 plans above cover the emulated ones; the workspace bound adds the emulation's scratch."""
+    layout, rank and flag set the plans with the same panel width are step-for-step identical, so
+    the gloo executions of the FP64 plans above cover the emulated ones; by default the emulation
+    takes wider panels (its per-product fixed costs); the workspace bound adds its scratch."""
     cases = [(mm.MM_ROW_BLOCK, (0, 0), f, w) for f in ROW_FLAGS for w in (1, 2, 3, 8)]
     cases += [(mm.MM_SUMMA_2D, g, 0, g[0] * g[1]) for g in ((1, 2), (2, 2), (2, 4))]
     cases += [(mm.MM_SUMMA_25D, (2, 2), mm.MM_REPLICATE, 8), (mm.MM_SUMMA_25D, (1, 2), mm.MM_REPLICATE, 4)]
     for layout, grid, flags, world in cases:
         for r in range(world):
             a = mm.shard_plan(1000, 3000, 777, torch.float64, layout=layout, grid=grid, flags=flags, world=world,
-                              rank=r)
+                              rank=r, panel=256)
             b = mm.shard_plan(1000, 3000, 777, torch.float64, layout=layout, grid=grid, flags=flags, world=world,
-                              rank=r, f64_emulation=True)
+                              rank=r, f64_emulation=True, panel=256)
             assert a == b, (layout, grid, flags, world, r)
+            gemms = [sum(st["op"] == "GEMM" for st in mm.shard_plan(20000, 30000, 7770, torch.float64, layout=layout,
+                                                                     grid=grid, flags=flags, world=world, rank=r,
+                                                                     f64_emulation=e)[0]) for e in (False, True)]
+            assert gemms[1] <= gemms[0], (layout, grid, flags, world, r, gemms)
         for lay in (layout,):
             plain = mm.workspace_size(1000, 3000, 777, torch.float64, lay, world)
             emu = mm.workspace_size(1000, 3000, 777, torch.float64, lay, world, f64_emulation=True)
