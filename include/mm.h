@@ -253,7 +253,8 @@ typedef struct {
 
 /* The plan rank r of G executes for mm_gemm_sharded(m, n, p, dtype, layout, grid_rows, grid_cols,
  * flags, root).  `panel`: column-panel width of the B broadcast (row-block) or k-panel width (SUMMA);
- * 0 = the library default.  Writes at most `cap` steps to `steps` (may be NULL with cap 0) and the
+ * 0 = the library default (p/8 and 2048; MM_F64_EMU: p/2 and 8192, each emulated panel product
+ * having fixed costs).  Writes at most `cap` steps to `steps` (may be NULL with cap 0) and the
  * plan's metadata to *info (required).  Returns MM_ERR_USAGE for invalid arguments (the same checks
  * as mm_gemm_sharded: dims >= 1, 0 <= r < G, root in range, grid consistent with G, flags valid for
  * the layout; SUMMA layouts for MM_F64 and MM_F64_EMU only).  Pure host logic. */
