@@ -22,7 +22,9 @@
  *                                               rebuilt by Chinese remaindering (Garner) and
  *                                               rounded once to binary64; exact for integer
  *                                               inputs, ~1e-17..1e-16 normalised error on U[-1,1)
- *                                               inputs; finite inputs only; n < 131072 (n·2^14 <
+ *                                               inputs; finite inputs only (an Inf / NaN is
+ *                                               reported by mm_sync_check, MM_ERR_RUNTIME, C
+ *                                               undefined); n < 131072 (n·2^14 <
  *                                               2^31 per INT32 sum); device scratch ≈
  *                                               N·(m·n + n·p + m·p) + 4·m·p bytes
  *                                               (mm_workspace_size); every layout of

@@ -60,7 +60,7 @@ struct mm_ctx {
     void* comm;  // ncclComm_t it is registered with
   };
   std::vector<Window> windows;
-  void* emu_buf = nullptr;    // MM_F64_EMU: digit planes of A and B, INT32 partial product, exponents
+  void* emu_buf = nullptr;    // MM_F64_EMU: residue planes of A, B and C, INT32 product, exponents
   size_t emu_bytes = 0;
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters

@@ -19,7 +19,8 @@
 //     by 2^-(2β - e_i - f_j) (exact unless the result is subnormal).
 // Accuracy: exact integer inputs give exact results (bit-identical to the oracle); U[-1,1) inputs
 // give normalised errors ~1e-17..1e-16, the accuracy class of DMMA (tests/test_gpu_parity.py).
-// Inputs must be finite.  Cost: N INT8 GEMMs (16 at C5) instead of DMMA's n/4 DMMA k-steps.
+// Inputs must be finite: an Inf or NaN is detected by the scale kernels and reported by
+// mm_sync_check (C is then undefined; IEEE propagation needs MM_F64).  Cost: N INT8 GEMMs (16 at C5) instead of DMMA's n/4 DMMA k-steps.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -154,11 +155,19 @@ __device__ __forceinline__ void limbs(double x, int& a2, int& a1, int& a0) {
   a2 = (int)(v >> 40);
 }
 
-// e[i] = bias + frexp exponent of max_k |A[i][k]| (0 if the row is zero)
-__global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int* __restrict__ e) {
+// e[i] = bias + frexp exponent of max_k |A[i][k]| (0 if the row is zero); an Inf / NaN operand
+// latches kErrNonFinite in the device error word (reported by mm_sync_check)
+__global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int* __restrict__ e,
+                               int* __restrict__ err) {
   const int64_t i = blockIdx.x;
   double mx = 0.0;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) mx = fmax(mx, fabs(A[i * lda + k]));
+  bool finite = true;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double x = A[i * lda + k];
+    finite &= isfinite(x);
+    mx = fmax(mx, fabs(x));
+  }
+  if (!finite) atomicCAS(err, 0, kErrNonFinite);
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -176,12 +185,18 @@ __global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_
 
 // f[j] = max over rows (atomicMax of the encoded exponent; f zeroed before)
 __global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t p, int64_t rows_per,
-                               int* __restrict__ f) {
+                               int* __restrict__ f, int* __restrict__ err) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= p) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
   double mx = 0.0;
-  for (int64_t k = r0; k < r1; ++k) mx = fmax(mx, fabs(B[k * ldb + j]));
+  bool finite = true;
+  for (int64_t k = r0; k < r1; ++k) {
+    const double x = B[k * ldb + j];
+    finite &= isfinite(x);
+    mx = fmax(mx, fabs(x));
+  }
+  if (!finite) atomicCAS(err, 0, kErrNonFinite);
   if (mx > 0.0) {
     int ex = 0;
     frexp(mx, &ex);
@@ -369,17 +384,19 @@ void launch_combine(const uint8_t* R, int64_t m, int64_t p, int64_t pp, double* 
 }
 
 template <int L>
-void reduce_at(const int4* S, int64_t count4, uint32_t* R, int sms, cudaStream_t s) {
-  reduce_mod_kernel<L><<<grid_for(count4, sms), 256, 0, s>>>(S, count4, R);
+void reduce_at(const int4* S, int64_t count4, uint32_t* R, int blocks, cudaStream_t s) {
+  reduce_mod_kernel<L><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, blocks)), 256, 0, s>>>(
+      S, count4, R);
 }
 
-void launch_reduce(int l, const int4* S, int64_t count4, uint32_t* R, int sms, cudaStream_t s) {
+// blocks: at most this many 256-thread blocks (grid-stride)
+void launch_reduce(int l, const int4* S, int64_t count4, uint32_t* R, int blocks, cudaStream_t s) {
   using Fn = void (*)(const int4*, int64_t, uint32_t*, int, cudaStream_t);
   static constexpr Fn fns[kMaxMod] = {reduce_at<0>,  reduce_at<1>,  reduce_at<2>,  reduce_at<3>,
                                       reduce_at<4>,  reduce_at<5>,  reduce_at<6>,  reduce_at<7>,
                                       reduce_at<8>,  reduce_at<9>,  reduce_at<10>, reduce_at<11>,
                                       reduce_at<12>, reduce_at<13>, reduce_at<14>, reduce_at<15>};
-  fns[l](S, count4, R, sms, s);
+  fns[l](S, count4, R, blocks, s);
 }
 
 }  // namespace
@@ -426,12 +443,12 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     return MM_OK;
   };
   // scales
-  row_exp_kernel<<<(unsigned)m, 256, 0, s>>>(A, lda, n, e);
+  row_exp_kernel<<<(unsigned)m, 256, 0, s>>>(A, lda, n, e, ctx->d_err);
   if ((st = chk("row exponents", 1)) != MM_OK) return st;
   if (cudaMemsetAsync(f, 0, (size_t)p * 4, s) != cudaSuccess) return set_err(ctx, MM_ERR_RUNTIME, "MM_F64_EMU memset failed");
   const int64_t rows_per = std::max<int64_t>(64, (n + 63) / 64);
   col_exp_kernel<<<dim3((unsigned)((p + 255) / 256), (unsigned)((n + rows_per - 1) / rows_per)), 256, 0, s>>>(B, ldb, n, p,
-                                                                                                           rows_per, f);
+                                                                                                           rows_per, f, ctx->d_err);
   if ((st = chk("column exponents", 1)) != MM_OK) return st;
   // residues of the scaled integers
   switch (L.nmod) {
@@ -440,13 +457,14 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     default: launch_residues<16>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
   }
   if ((st = chk("residues", 2)) != MM_OK) return st;
-  // one exact INT8 product per modulus, reduced to its residue
+  // one exact INT8 product per modulus, reduced to its residue bytes (a side-stream reduction
+  // overlapping the next product measured 0.80-0.96x: profiles/ab_emu_overlap_r2zz2.txt)
   for (int l = 0; l < L.nmod; ++l) {
     st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp, S, L.pp,
                  0, s);
     if (st != MM_OK) return st;
     launch_reduce(l, reinterpret_cast<const int4*>(S), m * L.pp / 4, reinterpret_cast<uint32_t*>(R + (int64_t)l * m * L.pp),
-                  sms, s);
+                  sms * 16, s);
     if ((st = chk("residue reduction", 1)) != MM_OK) return st;
   }
   // Chinese remaindering, scaling and the binary64 store

@@ -10,6 +10,9 @@
 namespace mmb {
 
 constexpr int kMaxDevices = 64;  // per-device launch state (function attributes, occupancy)
+// device error word value latched by MM_F64_EMU when an operand is Inf or NaN (the pipeline-wait
+// timeouts latch small positive codes)
+constexpr int kErrNonFinite = 0x4E4F4E46;
 
 // Problem as the kernels see it: C (M×N, leading dim ldc elements) = A (M×K) · B (K×N).
 // Paper notation: M = m, K = n, N = p.

@@ -773,6 +773,9 @@ __attribute__((visibility("default"))) mm_status mm_sync_check(mm_ctx* ctx, void
   if (h != 0) {
     cudaMemset(ctx->d_err, 0, 8 * sizeof(int));  // error word + wave-barrier / pacing counters
     if (ctx->sk_flags) cudaMemset(ctx->sk_flags, 0, ctx->sk_flag_count * sizeof(unsigned));
+    if (h == kErrNonFinite)
+      return set_err(ctx, MM_ERR_RUNTIME, "MM_F64_EMU: an operand holds Inf or NaN (the emulation needs finite "
+                                          "inputs; C is undefined — use MM_F64 for IEEE propagation)");
     return set_err(ctx, MM_ERR_RUNTIME, "device pipeline wait timed out (code %d)", h);
   }
   return MM_OK;

@@ -867,6 +867,26 @@ def test_f64_emulation_long_k(mm):
         mm.gemm(Ad, Bd, f64_emulation=True)
 
 
+def test_f64_emulation_non_finite_reported(mm):
+    """MM_F64_EMU cannot propagate Inf / NaN through integer arithmetic: an Inf in A or a NaN in B is
+    detected by the scale kernels and reported by mm_sync_check (MM_ERR_RUNTIME naming the cause);
+    the context stays usable (the next finite product is exact)."""
+    m, n, p = 64, 96, 80
+    A, B = gen("f64", "exact", 76, m, n, p, 2049)
+    for where in ("A", "B"):
+        Ab, Bb = A.copy(), B.copy()
+        if where == "A":
+            Ab[3, 5] = np.inf
+        else:
+            Bb[7, 2] = np.nan
+        mm.gemm(to_dev(Ab, "f64"), to_dev(Bb, "f64"), f64_emulation=True)
+        with pytest.raises(RuntimeError, match="Inf or NaN"):
+            mm.sync_check()
+    C = mm.gemm(to_dev(A, "f64"), to_dev(B, "f64"), f64_emulation=True)
+    mm.sync_check()
+    assert np.array_equal(C.cpu().numpy(), oracle.gemm_f64(A, B))
+
+
 def test_f64_emulation_config1_golden(mm):
     """C2x (configs[1] shape, K=2049 exact pin): the emulated product's full-output checksum equals
     SURVEY c7's golden, like DMMA's."""
