@@ -26,7 +26,7 @@
  *                                               reported by mm_sync_check, MM_ERR_RUNTIME, C
  *                                               undefined); n < 131072 (n·2^14 <
  *                                               2^31 per INT32 sum); device scratch ≈
- *                                               N·(m·n + n·p + m·p) + 4·m·p bytes
+ *                                               N·(m·n + n·p + m·p) bytes
  *                                               (mm_workspace_size); every layout of
  *                                               mm_gemm_sharded, its local products emulated)
  *   MM_S8_S32   int8     × int8     → int32    (INT32 accumulate, exact while

@@ -60,8 +60,9 @@ struct mm_ctx {
     void* comm;  // ncclComm_t it is registered with
   };
   std::vector<Window> windows;
-  void* emu_buf = nullptr;    // MM_F64_EMU: residue planes of A, B and C, INT32 product, exponents
+  void* emu_buf = nullptr;    // MM_F64_EMU: residue planes of A, B and C, exponents
   size_t emu_bytes = 0;
+  int res_mod = 0;  // MM_F64_EMU: its INT8 products store C mod res_mod as bytes (0 = INT32 C)
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   unsigned long long* clk_buf = nullptr;  // clock meter: 4096 CTAs x {c0, t0, c1, t1} of the last launch

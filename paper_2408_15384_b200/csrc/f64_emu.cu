@@ -10,7 +10,8 @@
 //     an integer input stays an integer after the scaling (2^(β-e) ≥ 1), so it is not rounded.
 //   * Residues.  N pairwise-coprime moduli m_1..m_N ≤ 256 (M = Π m_l); the symmetric residues
 //     a'_ik mod m_l, b'_kj mod m_l lie in [-128, 127], so each C'_l = A'_l · B'_l is one INT8
-//     product with INT32 accumulation, exact while n · 2^14 < 2^31 (n < 131072).
+//     product with INT32 accumulation, exact while n · 2^14 < 2^31 (n < 131072); the product's
+//     epilogue stores C'_l mod m_l as bytes (gemm_tc.cu, GemmArgs::res_m).
 //   * Reconstruction.  C' = A'·B' is an integer with |C'| ≤ n · 2^(2β); N and β are chosen so that
 //     n · 2^(2β) ≤ M/2 - 1 with β ≥ 53 (N = 14..16 for n < 131072).  Garner's algorithm turns the
 //     residues c_l = C'_l mod m_l into symmetric mixed-radix digits v_l (exact small-integer
@@ -48,7 +49,7 @@ struct CrtTab {
   int beta;                       // β
   int m[kMaxMod];                 // m_l
   // 0-based digits: C' = Σ_q v_q P_q with P_0 = 1, P_q = m[0] ... m[q-1]
-  int pmod[kMaxMod][kMaxMod];     // pmod[q][k] = P_q mod m[k] for q < k
+  int pmod[kMaxMod][kMaxMod];     // pmod[q][k] = P_q · (P_k)^-1 mod m[k] for q < k
   int pinv[kMaxMod];              // (P_k mod m[k])^-1 mod m[k]
 };
 
@@ -88,11 +89,13 @@ CrtTab make_tab(int nmod, int beta) {
   }
   for (int k = 0; k < kMaxMod; ++k) {
     int pk = 1 % kMods[k];  // P_0 mod m[k]
+    int pj[kMaxMod];
     for (int j = 0; j < k; ++j) {
-      t.pmod[j][k] = pk;  // P_j mod m[k]
+      pj[j] = pk;  // P_j mod m[k]
       pk = (int)((int64_t)pk * kMods[j] % kMods[k]);
     }
     t.pinv[k] = k == 0 ? 1 : inv_mod(pk, kMods[k]);  // pk = P_k mod m[k]
+    for (int j = 0; j < k; ++j) t.pmod[j][k] = (int)((int64_t)pj[j] * t.pinv[k] % kMods[k]);
   }
   return t;
 }
@@ -159,15 +162,17 @@ __device__ __forceinline__ void limbs(double x, int& a2, int& a1, int& a0) {
 // latches kErrNonFinite in the device error word (reported by mm_sync_check)
 __global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_t n, int* __restrict__ e,
                                int* __restrict__ err) {
-  const int64_t i = blockIdx.x;
+  const double* a = A + (int64_t)blockIdx.x * lda;
   double mx = 0.0;
-  bool finite = true;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-    const double x = A[i * lda + k];
-    finite &= isfinite(x);
+  int bad = 0;
+#pragma unroll 4
+  for (int k = threadIdx.x; k < (int)n; k += blockDim.x) {  // n < 2^17 (the emulation's bound)
+    const double x = a[k];
+    bad |= (__double2hiint(x) & 0x7FF00000) == 0x7FF00000;  // Inf or NaN: all exponent bits set
     mx = fmax(mx, fabs(x));
   }
-  if (!finite) atomicCAS(err, 0, kErrNonFinite);
+  if (bad) atomicCAS(err, 0, kErrNonFinite);
+  const int64_t i = blockIdx.x;
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -190,13 +195,13 @@ __global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_
   if (j >= p) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per, r1 = min(n, r0 + rows_per);
   double mx = 0.0;
-  bool finite = true;
+  int bad = 0;
   for (int64_t k = r0; k < r1; ++k) {
     const double x = B[k * ldb + j];
-    finite &= isfinite(x);
+    bad |= (__double2hiint(x) & 0x7FF00000) == 0x7FF00000;  // Inf or NaN
     mx = fmax(mx, fabs(x));
   }
-  if (!finite) atomicCAS(err, 0, kErrNonFinite);
+  if (bad) atomicCAS(err, 0, kErrNonFinite);
   if (mx > 0.0) {
     int ex = 0;
     frexp(mx, &ex);
@@ -249,24 +254,6 @@ __global__ void residues_b_kernel(const double* __restrict__ B, int64_t ldb, int
   }
 }
 
-// R[i*pp + j] = S[i*pp + j] mod m_L in [0, m_L) (S: the exact INT32 product of the residues), 4 per thread
-template <int L>
-__global__ void reduce_mod_kernel(const int4* __restrict__ S, int64_t count4, uint32_t* __restrict__ R) {
-  constexpr int m = mod_at(L);
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < count4; w += (int64_t)gridDim.x * blockDim.x) {
-    const int4 v = S[w];
-    const int s[4] = {v.x, v.y, v.z, v.w};
-    uint32_t word = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      // |s| < 2^31: split s = 2^16 h + lo, h signed, lo in [0, 2^16) (2^16 mod m is a constant)
-      const int h = s[c] >> 16, lo = s[c] & 0xFFFF;
-      word |= (uint32_t)mod_of(h * (int)((1u << 16) % (uint32_t)m) + lo, m) << (8 * c);
-    }
-    R[w] = word;
-  }
-}
-
 // double-double t·M + v (M < 2^24, |v| < 2^24): Horner step of the mixed-radix value
 __device__ __forceinline__ void dd_step(double& hi, double& lo, double m, double v) {
   const double p = hi * m;
@@ -296,17 +283,18 @@ __global__ void __launch_bounds__(256) crt_combine_kernel(const uint8_t* __restr
     uint32_t word[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) word[k] = __ldg(r + k * (plane / 4));
-    // Garner: v_k = (c_k - Σ_{q<k} v_q (P_q mod m_k)) · (P_k mod m_k)^-1 mod m_k, symmetric digits
+    // Garner: v_k = (c_k - Σ_{q<k} v_q P_q) · P_k^-1 mod m_k = c_k·P_k^-1 - Σ_{q<k} v_q·(P_q P_k^-1 mod m_k)
+    // mod m_k (tables folded: one reduction per digit), symmetric digits
     int v[4][N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const int mk = mod_at(k);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        int x = (int)((word[k] >> (8 * c)) & 0xFF);
+        int x = (int)((word[k] >> (8 * c)) & 0xFF) * t.pinv[k];
 #pragma unroll
-        for (int q = 0; q < k; ++q) x -= v[c][q] * t.pmod[q][k];  // |x| < 2^19
-        const int d = mod_of(mod_of(x, mk) * t.pinv[k], mk);
+        for (int q = 0; q < k; ++q) x -= v[c][q] * t.pmod[q][k];  // |x| < 2^16 + 15·128·256 < 2^20
+        const int d = mod_of(x, mk);
         v[c][k] = d > (mk >> 1) ? d - mk : d;  // 256: [-127, 128]; odd: [-(m-1)/2, (m-1)/2]
       }
     }
@@ -352,7 +340,7 @@ inline size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 struct Layout {
   int nmod, beta;
   int64_t kp, pp;
-  size_t a_bytes, b_bytes, s_bytes, r_bytes, e_bytes, f_bytes, total;
+  size_t a_bytes, b_bytes, r_bytes, e_bytes, f_bytes, total;
 };
 
 bool layout_for(int64_t m, int64_t n, int64_t p, Layout* L) {
@@ -361,11 +349,10 @@ bool layout_for(int64_t m, int64_t n, int64_t p, Layout* L) {
   L->pp = (p + 15) / 16 * 16;
   L->a_bytes = up256((size_t)(L->nmod * m * L->kp));
   L->b_bytes = up256((size_t)(L->nmod * n * L->pp));
-  L->s_bytes = up256((size_t)(m * L->pp * 4));
   L->r_bytes = up256((size_t)(L->nmod * m * L->pp));
   L->e_bytes = up256((size_t)m * 4);
   L->f_bytes = up256((size_t)p * 4);
-  L->total = L->a_bytes + L->b_bytes + L->s_bytes + L->r_bytes + L->e_bytes + L->f_bytes;
+  L->total = L->a_bytes + L->b_bytes + L->r_bytes + L->e_bytes + L->f_bytes;
   return true;
 }
 
@@ -381,22 +368,6 @@ template <int N>
 void launch_combine(const uint8_t* R, int64_t m, int64_t p, int64_t pp, double* C, int64_t ldc, const int* e,
                     const int* f, int beta_one, const CrtTab& t, int sms, cudaStream_t s) {
   crt_combine_kernel<N><<<grid_for(m * ((p + 3) / 4), sms), 256, 0, s>>>(R, m, p, pp, C, ldc, e, f, beta_one, t);
-}
-
-template <int L>
-void reduce_at(const int4* S, int64_t count4, uint32_t* R, int blocks, cudaStream_t s) {
-  reduce_mod_kernel<L><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((count4 + 255) / 256, blocks)), 256, 0, s>>>(
-      S, count4, R);
-}
-
-// blocks: at most this many 256-thread blocks (grid-stride)
-void launch_reduce(int l, const int4* S, int64_t count4, uint32_t* R, int blocks, cudaStream_t s) {
-  using Fn = void (*)(const int4*, int64_t, uint32_t*, int, cudaStream_t);
-  static constexpr Fn fns[kMaxMod] = {reduce_at<0>,  reduce_at<1>,  reduce_at<2>,  reduce_at<3>,
-                                      reduce_at<4>,  reduce_at<5>,  reduce_at<6>,  reduce_at<7>,
-                                      reduce_at<8>,  reduce_at<9>,  reduce_at<10>, reduce_at<11>,
-                                      reduce_at<12>, reduce_at<13>, reduce_at<14>, reduce_at<15>};
-  fns[l](S, count4, R, blocks, s);
 }
 
 }  // namespace
@@ -430,8 +401,7 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
   uint8_t* base = static_cast<uint8_t*>(ctx->emu_buf);
   int8_t* Ar = reinterpret_cast<int8_t*>(base);
   int8_t* Br = reinterpret_cast<int8_t*>(base + L.a_bytes);
-  int32_t* S = reinterpret_cast<int32_t*>(base + L.a_bytes + L.b_bytes);
-  uint8_t* R = base + L.a_bytes + L.b_bytes + L.s_bytes;
+  uint8_t* R = base + L.a_bytes + L.b_bytes;
   int* e = reinterpret_cast<int*>(R + L.r_bytes);
   int* f = reinterpret_cast<int*>(R + L.r_bytes + L.e_bytes);
   const CrtTab t = make_tab(L.nmod, L.beta);
@@ -457,16 +427,20 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     default: launch_residues<16>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
   }
   if ((st = chk("residues", 2)) != MM_OK) return st;
-  // one exact INT8 product per modulus, reduced to its residue bytes (a side-stream reduction
-  // overlapping the next product measured 0.80-0.96x: profiles/ab_emu_overlap_r2zz2.txt)
+  // One exact INT8 product per modulus; its epilogue stores the INT32 values mod m_l as bytes
+  // straight into residue plane l (ctx->res_mod; a separate INT32 array + reduction kernel cost
+  // 8.7 % of an 8192^3 product)
+  struct ResetResMod {
+    mm_ctx* c;
+    ~ResetResMod() { c->res_mod = 0; }
+  } reset{ctx};
   for (int l = 0; l < L.nmod; ++l) {
-    st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp, S, L.pp,
-                 0, s);
+    ctx->res_mod = t.m[l];
+    st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp,
+                 R + (int64_t)l * m * L.pp, L.pp, 0, s);
     if (st != MM_OK) return st;
-    launch_reduce(l, reinterpret_cast<const int4*>(S), m * L.pp / 4, reinterpret_cast<uint32_t*>(R + (int64_t)l * m * L.pp),
-                  sms * 16, s);
-    if ((st = chk("residue reduction", 1)) != MM_OK) return st;
   }
+  ctx->res_mod = 0;
   // Chinese remaindering, scaling and the binary64 store
   switch (L.nmod) {
     case 14: launch_combine<14>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;

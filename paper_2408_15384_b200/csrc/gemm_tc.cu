@@ -450,6 +450,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ebuf = sEpi + ew * 4096u;
     uint32_t n_stores = 0;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0, bool red = false) {
+      if (args.res_m) {
+        // MM_F64_EMU: the exact INT32 values reduced mod res_m to bytes — x = 2^16 h + l, y = h·(2^16
+        // mod m) + l ≡ x (|y| < 2^24, exact in float), r = y − m·floor(y/m) corrected — 32 bytes per
+        // row, staged unswizzled (32 rows × 32 B) and stored by one TMA store (uint8 map, no reduce-add)
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int x = (int)v[4 * i + u];
+            const int y = (x >> 16) * args.res_c16 + (x & 0xFFFF);
+            int r = y - __float2int_rd(__int2float_rn(y) * args.res_rcp) * args.res_m;
+            r += r < 0 ? args.res_m : 0;
+            r -= r >= args.res_m ? args.res_m : 0;
+            word |= (uint32_t)r << (8 * u);
+          }
+          w[i] = word;
+        }
+        if (n_stores >= 1) {
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        st_shared_v4(ebuf + lane * 32u, w[0], w[1], w[2], w[3]);
+        st_shared_v4(ebuf + lane * 32u + 16u, w[4], w[5], w[6], w[7]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, ebuf, (int32_t)col0, (int32_t)row_base);
+          bulk_commit();
+        }
+        ++n_stores;
+        return;
+      }
       if (args.c_tma) {
         const uint64_t c0 = args.trace ? clock64() : 0;
         if (n_stores >= 1) {

@@ -104,7 +104,9 @@ mm_status encode_2d(mm_ctx* ctx, CUtensorMap* map, CUtensorMapDataType dt, size_
   cuuint32_t boxd[2] = {box[0], box[1]};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   swizzle_bytes == 0    ? CU_TENSOR_MAP_SWIZZLE_NONE
+                   : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                         : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(ctx, MM_ERR_UNSUPPORTED, "TMA encode failed for %s (%lld x %lld, ld %lld): CUresult %d", what,
@@ -291,6 +293,9 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
   a.debug = 0;
   a.ka = 1;
   a.clk = ctx->clk_on ? ctx->clk_buf : nullptr;
+  a.res_m = 0;
+  a.res_c16 = 0;
+  a.res_rcp = 0.0f;
 #ifdef MM_DIAG
   if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
@@ -431,6 +436,18 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     // C through TMA stores when its base and pitch allow (else predicated register stores)
     CUtensorMap tmC;
     memset(&tmC, 0, sizeof tmC);
+    if (ctx->res_mod) {  // MM_F64_EMU's products: C mod res_mod as bytes (uint8 C, TMA stores only)
+      if (!i8 || !tma_ok(C, ldc, 1))
+        return set_err(ctx, MM_ERR_RUNTIME, "internal: residue output needs an INT8 product and a TMA-storable C");
+      a.res_m = ctx->res_mod;
+      a.res_c16 = (int)(65536u % (unsigned)ctx->res_mod);
+      a.res_rcp = 1.0f / (float)ctx->res_mod;
+      a.no_reduce = 1;  // partial sums are added before the reduction, never in C
+      a.c_tma = 1;
+      const uint32_t rbox[2] = {32, 32};
+      st = encode_2d(ctx, &tmC, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, C, m, p, ldc, rbox, "C residues", 0);
+      if (st != MM_OK) return st;
+    } else {
     a.c_tma = tma_ok(C, ldc, 4) ? 1 : 0;
     if (const char* env = knob("MM_TMA_STORE")) a.c_tma = a.c_tma && atoi(env) != 0;  // tuning knob
     if (a.c_tma) {
@@ -438,6 +455,7 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
       st = encode_2d(ctx, &tmC, i8 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, m, p, ldc,
                      cbox, "C");
       if (st != MM_OK) return st;
+    }
     }
     // B for N-half tail items: bf16 — the same map (a 64-column box is 128 B); int8 — 64-column
     // (64-B) boxes, 64-byte swizzle
