@@ -15,14 +15,15 @@
 //   * Reconstruction.  C' = A'·B' is an integer with |C'| ≤ n · 2^(2β); N and β are chosen so that
 //     n · 2^(2β) ≤ M/2 - 1 with β ≥ 53 (N = 14..16 for n < 131072).  Garner's algorithm turns the
 //     residues c_l = C'_l mod m_l into symmetric mixed-radix digits v_l (exact small-integer
-//     arithmetic), C' = v_1 + m_1 (v_2 + m_2 (v_3 + ...)), evaluated by Horner's rule in
-//     double-double (exact while below 2^106 relative error), rounded once to binary64 and scaled
+//     arithmetic), C' = v_1 + m_1 (v_2 + m_2 (v_3 + ...)), evaluated by Horner's rule over digit
+//     triples, plain binary64 while exact, then double-double (~2^-104 relative), rounded once to binary64 and scaled
 //     by 2^-(2β - e_i - f_j) (exact unless the result is subnormal).
 // Accuracy: exact integer inputs give exact results (bit-identical to the oracle); U[-1,1) inputs
 // give normalised errors ~1e-17..1e-16, the accuracy class of DMMA (tests/test_gpu_parity.py).
 // Inputs must be finite: an Inf or NaN is detected by the scale kernels and reported by
-// mm_sync_check (C is then undefined; IEEE propagation needs MM_F64).  Cost: N INT8 GEMMs (16 at C5) instead of DMMA's n/4 DMMA k-steps.
-#include <cfloat>
+// mm_sync_check (C is then undefined; IEEE propagation needs MM_F64).
+// Cost: N INT8 products (16 at C5) + O(N·(mn + np) + N²·mp) integer work in the residue and
+// reconstruction kernels; DESIGN.md §6 K5 has the measured breakdown.
 #include <climits>
 #include <cmath>
 #include <cstdint>
