@@ -3,6 +3,7 @@ seams: multiples of 16/32/64/128/256 and one off), dtypes and schedule knobs (ta
 modes, tile widths, K atoms per stage, CTA pairs, cluster multicast, FP64 tile and split),
 exact-integer inputs so every comparison is bit-exact in any summation order
 (SURVEY 8(c) c4).  Each case also runs with a guard-banded output (no store outside C).
+MM_F64_EMU is fuzzed the same way (its INT8 products under random knobs).
 """
 import os
 import random
@@ -144,6 +145,57 @@ def test_fuzz_random_values(mm, case):
         mm.sync_check()
         err = oracle.normalized_error(C.cpu().numpy(), Cref, D)
         assert err <= tol, (err, env)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _cases_emu():
+    rng = random.Random(20261021)
+    out = []
+    for i in range(32):
+        m, n, p = _dim(rng), _dim(rng), _dim(rng)
+        if i % 8 == 7:
+            n = rng.randint(20000, 70000)  # long K: INT32 sums of residue products near their bound
+            m, p = rng.randint(1, 64), rng.randint(1, 64)
+        env = {k: rng.choice(v) for k, v in KNOBS_TC.items()}
+        out.append((i, m, n, p, {k: v for k, v in env.items() if v is not None}))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases_emu(), ids=lambda c: f"e{c[0]}-{c[1]}x{c[2]}x{c[3]}")
+def test_fuzz_f64_emulation(mm, case):
+    """MM_F64_EMU under random shapes and random schedule knobs of its INT8 products (their
+    epilogue writes residue bytes; a forced reduce-add tail must fall back): exact-integer inputs
+    bit-exact against the oracle with a guard-banded output, then U[-1,1) inputs with rows and
+    columns scaled by random powers of two within the FP64 tolerance and DMMA's ~1e-16 class."""
+    i, m, n, p, env = case
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        A, B = _gen("f64", 900 + i, m, n, p)
+        Cref = _ref("f64", A, B)
+        guard = 4096
+        buf = torch.full((guard + m * p + guard,), -7.0, dtype=torch.float64, device="cuda")
+        C = buf[guard:guard + m * p].view(m, p)
+        C.fill_(5.0)
+        mm.gemm(_dev(A, "f64"), _dev(B, "f64"), out=C, f64_emulation=True)
+        mm.sync_check()
+        h = buf.cpu().numpy()
+        assert np.all(h[:guard] == -7) and np.all(h[guard + m * p:] == -7), ("store outside C", env)
+        bad = int((C.cpu().numpy() != Cref).sum())
+        assert bad == 0, (f"{bad} mismatches", env)
+        rng = np.random.default_rng(900 + i)
+        A = sg.uniform_f64(950 + i, 1, m, n) * np.ldexp(1.0, rng.integers(-60, 60, m))[:, None]
+        B = sg.uniform_f64(950 + i, 2, n, p) * np.ldexp(1.0, rng.integers(-60, 60, p))[None, :]
+        Cref, D = oracle.gemm_f64(A, B), oracle.absden_f64(A, B)
+        C = mm.gemm(_dev(A, "f64"), _dev(B, "f64"), f64_emulation=True)
+        mm.sync_check()
+        err = oracle.normalized_error(C.cpu().numpy(), Cref, D)
+        assert err <= 1e-12 and err <= 1e-15, (err, env)
     finally:
         for k, v in saved.items():
             if v is None:
