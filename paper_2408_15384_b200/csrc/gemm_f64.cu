@@ -88,10 +88,10 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB, CK>::THREADS, 1
   // item stored, [6] exit
   unsigned long long* tl = args.trace ? args.trace + (size_t)blockIdx.x * 8 : nullptr;
   if (tl && threadIdx.x == 0) tl[0] = globaltimer_ns();
-  uint64_t clk_c0 = 0, clk_t0 = 0;  // clock meter (mm_clock_meter)
-  if (args.clk && threadIdx.x == 0) {
-    clk_c0 = clock64();
-    clk_t0 = globaltimer_ns();
+  // clock meter (mm_clock_meter): entry stamps stored at once (no register held over the kernel)
+  if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
+    args.clk[4 * (size_t)blockIdx.x] = clock64();
+    args.clk[4 * (size_t)blockIdx.x + 1] = globaltimer_ns();
   }
   constexpr int NCONS = Cfg::NCONS;
   constexpr int NTILE = Cfg::NTILE;
@@ -447,8 +447,6 @@ __global__ void __launch_bounds__(F64Cfg<BM, BN, WM, WN, KS, KB, CK>::THREADS, 1
   if (tl && threadIdx.x == 0) tl[6] = globaltimer_ns();
   if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
     unsigned long long* r = args.clk + 4 * (size_t)blockIdx.x;
-    r[0] = clk_c0;
-    r[1] = clk_t0;
     r[2] = clock64();
     r[3] = globaltimer_ns();
   }

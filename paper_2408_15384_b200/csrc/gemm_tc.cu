@@ -149,10 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = TcCfg<I8, CG, NT, MC, KA>;
   const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
   // clock meter (mm_clock_meter): SM cycles and nanoseconds over this CTA's life
-  uint64_t clk_c0 = 0, clk_t0 = 0;
-  if (args.clk && threadIdx.x == 0) {
-    clk_c0 = clock64();
-    clk_t0 = globaltimer_ns();
+  // (entry stamps stored at once: no register held over the kernel)
+  if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
+    args.clk[4 * (size_t)blockIdx.x] = clock64();
+    args.clk[4 * (size_t)blockIdx.x + 1] = globaltimer_ns();
   }
   // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
   unsigned long long* tl = args.trace ? args.trace + 4096 * 16 + (size_t)blockIdx.x * 32 : nullptr;
@@ -766,8 +766,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
     unsigned long long* r = args.clk + 4 * (size_t)blockIdx.x;
-    r[0] = clk_c0;
-    r[1] = clk_t0;
     r[2] = clock64();
     r[3] = globaltimer_ns();
   }
