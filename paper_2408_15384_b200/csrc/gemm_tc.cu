@@ -149,10 +149,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = TcCfg<I8, CG, NT, MC, KA>;
   const uint64_t tr_entry = args.trace ? globaltimer_ns() : 0;
   // clock meter (mm_clock_meter): SM cycles and nanoseconds over this CTA's life
-  // (entry stamps stored at once: no register held over the kernel)
-  if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
-    args.clk[4 * (size_t)blockIdx.x] = clock64();
-    args.clk[4 * (size_t)blockIdx.x + 1] = globaltimer_ns();
+  // (held in registers: storing them at entry raised the BF16 pair kernel from 151 to 160 registers)
+  uint64_t clk_c0 = 0, clk_t0 = 0;
+  if (args.clk && threadIdx.x == 0) {
+    clk_c0 = clock64();
+    clk_t0 = globaltimer_ns();
   }
   // timeline (MM_TRACE): per CTA, items 0..7: MMA first issue / last issue, epilogue start / end
   unsigned long long* tl = args.trace ? args.trace + 4096 * 16 + (size_t)blockIdx.x * 32 : nullptr;
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ebuf = sEpi + ew * 4096u;
     uint32_t n_stores = 0;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0, bool red = false) {
-      if (args.res_m) {
+      if (I8 && args.res_m) {  // (compiled into the INT8 kernels only)
         // MM_F64_EMU: the exact INT32 values reduced mod res_m to bytes — x = 2^16 h + l, y = h·(2^16
         // mod m) + l ≡ x (|y| < 2^24, exact in float), r = y − m·floor(y/m) corrected — 32 bytes per
         // row, staged unswizzled (32 rows × 32 B) and stored by one TMA store (uint8 map, no reduce-add)
@@ -766,6 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (args.clk && threadIdx.x == 0 && blockIdx.x < 4096) {
     unsigned long long* r = args.clk + 4 * (size_t)blockIdx.x;
+    r[0] = clk_c0;
+    r[1] = clk_t0;
     r[2] = clock64();
     r[3] = globaltimer_ns();
   }
