@@ -139,9 +139,13 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None,
     return out
 
 
-def gemm_host(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, device: int = 0) -> torch.Tensor:
-    """C = A·B with host operands (copies in, computes, copies out; synchronous)."""
+def gemm_host(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, device: int = 0,
+              f64_emulation: bool = False) -> torch.Tensor:
+    """C = A·B with host operands (copies in, computes, copies out; synchronous);
+    f64_emulation (float64 operands): each block as MM_F64_EMU."""
     m, n, p, dt = _check_operands(A, B)
+    if f64_emulation:
+        dt = _dtype_code(A.dtype, True)
     if A.is_cuda or B.is_cuda:
         raise ValueError("gemm_host expects host tensors")
     if out is None:

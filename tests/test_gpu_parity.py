@@ -574,6 +574,16 @@ def test_host_operand_path(mm):
         check(dt, C.numpy(), Cref, D, exact=True)
 
 
+def test_host_operand_path_f64_emulated(mm):
+    """mm_gemm_host with MM_F64_EMU at a size the host path splits into 4 x 4 blocks (operands above
+    64 MB): every block is its own emulated product (ragged last blocks); exact-integer inputs
+    bit-exact against the oracle."""
+    m, n, p = 2600, 1900, 2300
+    A, B = gen("f64", "exact", 14, m, n, p, 2049)
+    C = mm.gemm_host(torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory(), f64_emulation=True)
+    assert np.array_equal(C.numpy(), oracle.gemm_f64(A, B))
+
+
 # ------------------------------------------------------------------ BASELINE.json configs, full size
 with open(os.path.join(GOLDEN, "oracle_fullsize.json")) as f:
     FULL = json.load(f)
