@@ -63,6 +63,9 @@ struct mm_ctx {
   void* emu_buf = nullptr;    // MM_F64_EMU: residue planes of A, B and C, exponents
   size_t emu_bytes = 0;
   int res_mod = 0;  // MM_F64_EMU: its INT8 products store C mod res_mod as bytes (0 = INT32 C)
+  int res_nbat = 0;  // > 1: one launch for res_nbat batches stacked along M (moduli res_mods[b])
+  int res_mods[16] = {};
+  int64_t res_bat_rows = 0, res_bat_krows = 0;  // rows per batch of A / C and of B
   void* bar_buf = nullptr;   // one int for the communicator barrier
   void* trace_buf = nullptr;  // MM_TRACE per-CTA counters
   unsigned long long* clk_buf = nullptr;  // clock meter: 4096 CTAs x {c0, t0, c1, t1} of the last launch

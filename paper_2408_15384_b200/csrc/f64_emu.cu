@@ -10,8 +10,9 @@
 //     an integer input stays an integer after the scaling (2^(β-e) ≥ 1), so it is not rounded.
 //   * Residues.  N pairwise-coprime moduli m_1..m_N ≤ 256 (M = Π m_l); the symmetric residues
 //     a'_ik mod m_l, b'_kj mod m_l lie in [-128, 127], so each C'_l = A'_l · B'_l is one INT8
-//     product with INT32 accumulation, exact while n · 2^14 < 2^31 (n < 131072); the product's
-//     epilogue stores C'_l mod m_l as bytes (gemm_tc.cu, GemmArgs::res_m).
+//     product with INT32 accumulation, exact while n · 2^14 < 2^31 (n < 131072); all N run as one
+//     batched launch (planes stacked along M) whose epilogue stores C'_l mod m_l as bytes
+//     (gemm_tc.cu, GemmArgs::res_m / bat_rows).
 //   * Reconstruction.  C' = A'·B' is an integer with |C'| ≤ n · 2^(2β); N and β are chosen so that
 //     n · 2^(2β) ≤ M/2 - 1 with β ≥ 53 (N = 14..16 for n < 131072).  Garner's algorithm turns the
 //     residues c_l = C'_l mod m_l into symmetric mixed-radix digits v_l (exact small-integer
@@ -210,47 +211,49 @@ __global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_
   }
 }
 
-// A residue planes: Ar[(l*m + i)*kp + k] = a'_ik mod m_l (k >= n: 0); 4 consecutive k per thread
+// A residue planes: Ar[(l*mp + i)*kp + k] = a'_ik mod m_l (k >= n or i >= m: 0 — the planes are
+// stacked along M in whole 256-row tiles for the batched product); 4 consecutive k per thread
 template <int N>
-__global__ void residues_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, int64_t kp,
-                                  const int* __restrict__ e, int beta, int8_t* __restrict__ Ar) {
+__global__ void residues_a_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t mp, int64_t n,
+                                  int64_t kp, const int* __restrict__ e, int beta, int8_t* __restrict__ Ar) {
   const int64_t q4 = kp / 4;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * q4; w += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < mp * q4; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = w / q4, k0 = (w % q4) * 4;
-    const int sc = beta - dec_exp(e[i]);
+    const int sc = i < m ? beta - dec_exp(e[i]) : 0;
     const double s1 = pow2(sc / 2), s2 = pow2(sc - sc / 2);  // scale2, hoisted
     int a2[4], a1[4], a0[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) limbs(k0 + c < n ? A[i * lda + k0 + c] * s1 * s2 : 0.0, a2[c], a1[c], a0[c]);
+    for (int c = 0; c < 4; ++c)
+      limbs(i < m && k0 + c < n ? A[i * lda + k0 + c] * s1 * s2 : 0.0, a2[c], a1[c], a0[c]);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       uint32_t word = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) word |= (uint32_t)(uint8_t)(int8_t)sym_residue(a2[c], a1[c], a0[c], mod_at(l)) << (8 * c);
-      *reinterpret_cast<uint32_t*>(Ar + ((int64_t)l * m + i) * kp + k0) = word;
+      *reinterpret_cast<uint32_t*>(Ar + ((int64_t)l * mp + i) * kp + k0) = word;
     }
   }
 }
 
-// B residue planes: Br[(l*n + k)*pp + j] = b'_kj mod m_l (j >= p: 0); 4 consecutive j per thread
+// B residue planes: Br[(l*kp + k)*pp + j] = b'_kj mod m_l (j >= p or k >= n: 0); 4 consecutive j per thread
 template <int N>
-__global__ void residues_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t p, int64_t pp,
-                                  const int* __restrict__ f, int beta, int8_t* __restrict__ Br) {
+__global__ void residues_b_kernel(const double* __restrict__ B, int64_t ldb, int64_t n, int64_t kp, int64_t p,
+                                  int64_t pp, const int* __restrict__ f, int beta, int8_t* __restrict__ Br) {
   const int64_t q4 = pp / 4;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n * q4; w += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < kp * q4; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = w / q4, j0 = (w % q4) * 4;
     int a2[4], a1[4], a0[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int64_t j = j0 + c;
-      limbs(j < p ? scale2(B[k * ldb + j], beta - dec_exp(f[j])) : 0.0, a2[c], a1[c], a0[c]);
+      limbs(j < p && k < n ? scale2(B[k * ldb + j], beta - dec_exp(f[j])) : 0.0, a2[c], a1[c], a0[c]);
     }
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       uint32_t word = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) word |= (uint32_t)(uint8_t)(int8_t)sym_residue(a2[c], a1[c], a0[c], mod_at(l)) << (8 * c);
-      *reinterpret_cast<uint32_t*>(Br + ((int64_t)l * n + k) * pp + j0) = word;
+      *reinterpret_cast<uint32_t*>(Br + ((int64_t)l * kp + k) * pp + j0) = word;
     }
   }
 }
@@ -270,14 +273,14 @@ __device__ __forceinline__ void dd_step(double& hi, double& lo, double m, double
 // C[i][j] (+)= 2^-(2β - e_i - f_j) · C'_ij, C' from its residues R_l by Garner + double-double Horner;
 // 4 consecutive j per thread (4-byte residue loads, the 4 elements' arithmetic interleaved), pp % 4 == 0
 template <int N>
-__global__ void __launch_bounds__(256) crt_combine_kernel(const uint8_t* __restrict__ R, int64_t m, int64_t p,
-                                                          int64_t pp, double* __restrict__ C, int64_t ldc,
+__global__ void __launch_bounds__(256) crt_combine_kernel(const uint8_t* __restrict__ R, int64_t m, int64_t mp,
+                                                          int64_t p, int64_t pp, double* __restrict__ C, int64_t ldc,
                                                           const int* __restrict__ e, const int* __restrict__ f,
                                                           int beta_one, const __grid_constant__ CrtTab t) {
   constexpr int G = (N + 2) / 3;                  // digit triples (the last may be short)
   constexpr int kTopBits = 8 * (N - 3 * (G - 1));  // bits of the top triple's value
   constexpr int kPlain = (53 - kTopBits) / 24;    // Horner steps exact in binary64
-  const int64_t plane = m * pp, q4 = (p + 3) / 4;
+  const int64_t plane = mp * pp, q4 = (p + 3) / 4;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < m * q4; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = w / q4, j0 = (w % q4) * 4;
     const uint32_t* r = reinterpret_cast<const uint32_t*>(R + i * pp + j0);
@@ -340,17 +343,18 @@ inline size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Layout {
   int nmod, beta;
-  int64_t kp, pp;
+  int64_t mp, kp, pp;  // rows per A / C plane (whole 256-row tiles), K and p padded to 16
   size_t a_bytes, b_bytes, r_bytes, e_bytes, f_bytes, total;
 };
 
 bool layout_for(int64_t m, int64_t n, int64_t p, Layout* L) {
   if (!crt_plan(n, &L->nmod, &L->beta)) return false;
+  L->mp = (m + 255) / 256 * 256;
   L->kp = (n + 15) / 16 * 16;
   L->pp = (p + 15) / 16 * 16;
-  L->a_bytes = up256((size_t)(L->nmod * m * L->kp));
-  L->b_bytes = up256((size_t)(L->nmod * n * L->pp));
-  L->r_bytes = up256((size_t)(L->nmod * m * L->pp));
+  L->a_bytes = up256((size_t)(L->nmod * L->mp * L->kp));
+  L->b_bytes = up256((size_t)(L->nmod * L->kp * L->pp));
+  L->r_bytes = up256((size_t)(L->nmod * L->mp * L->pp));
   L->e_bytes = up256((size_t)m * 4);
   L->f_bytes = up256((size_t)p * 4);
   L->total = L->a_bytes + L->b_bytes + L->r_bytes + L->e_bytes + L->f_bytes;
@@ -361,14 +365,14 @@ template <int N>
 void launch_residues(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t m, int64_t n, int64_t p,
                      const Layout& L, const int* e, const int* f, int8_t* Ar, int8_t* Br, const CrtTab& t, int sms,
                      cudaStream_t s) {
-  residues_a_kernel<N><<<grid_for(m * (L.kp / 4), sms), 256, 0, s>>>(A, lda, m, n, L.kp, e, t.beta, Ar);
-  residues_b_kernel<N><<<grid_for(n * (L.pp / 4), sms), 256, 0, s>>>(B, ldb, n, p, L.pp, f, t.beta, Br);
+  residues_a_kernel<N><<<grid_for(L.mp * (L.kp / 4), sms), 256, 0, s>>>(A, lda, m, L.mp, n, L.kp, e, t.beta, Ar);
+  residues_b_kernel<N><<<grid_for(L.kp * (L.pp / 4), sms), 256, 0, s>>>(B, ldb, n, L.kp, p, L.pp, f, t.beta, Br);
 }
 
 template <int N>
-void launch_combine(const uint8_t* R, int64_t m, int64_t p, int64_t pp, double* C, int64_t ldc, const int* e,
-                    const int* f, int beta_one, const CrtTab& t, int sms, cudaStream_t s) {
-  crt_combine_kernel<N><<<grid_for(m * ((p + 3) / 4), sms), 256, 0, s>>>(R, m, p, pp, C, ldc, e, f, beta_one, t);
+void launch_combine(const uint8_t* R, int64_t m, int64_t mp, int64_t p, int64_t pp, double* C, int64_t ldc,
+                    const int* e, const int* f, int beta_one, const CrtTab& t, int sms, cudaStream_t s) {
+  crt_combine_kernel<N><<<grid_for(m * ((p + 3) / 4), sms), 256, 0, s>>>(R, m, mp, p, pp, C, ldc, e, f, beta_one, t);
 }
 
 }  // namespace
@@ -428,25 +432,42 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     default: launch_residues<16>(A, lda, B, ldb, m, n, p, L, e, f, Ar, Br, t, sms, s); break;
   }
   if ((st = chk("residues", 2)) != MM_OK) return st;
-  // One exact INT8 product per modulus; its epilogue stores the INT32 values mod m_l as bytes
-  // straight into residue plane l (ctx->res_mod; a separate INT32 array + reduction kernel cost
-  // 8.7 % of an 8192^3 product)
-  struct ResetResMod {
+  // The N exact INT8 products; their epilogue stores C'_l mod m_l as bytes straight into residue
+  // plane l (ctx->res_*; an INT32 array + a reduction pass cost 8.7 % of an 8192^3 product).
+  // Products of less than two waves of 256-wide tiles run as ONE batched launch — the A planes
+  // stacked along M (batch l = rows [l·mp, (l+1)·mp)), each batch reading its own B plane: no N
+  // launches of a partial wave each (C2 shape 1.44x, 2048^3 1.24x, 1024^3 1.77x); larger ones as N
+  // launches, which the batched form did not beat (4096^3-32768^3: 0.95-0.99x,
+  // profiles/ab_emu_batched_r2zz14.txt)
+  struct ResetRes {
     mm_ctx* c;
-    ~ResetResMod() { c->res_mod = 0; }
+    ~ResetRes() { c->res_mod = 0; c->res_nbat = 0; }
   } reset{ctx};
-  for (int l = 0; l < L.nmod; ++l) {
-    ctx->res_mod = t.m[l];
-    st = gemm_ld(ctx, m, n, p, MM_S8_S32, Ar + (int64_t)l * m * L.kp, L.kp, Br + (int64_t)l * n * L.pp, L.pp,
-                 R + (int64_t)l * m * L.pp, L.pp, 0, s);
+  const int64_t tiles_one = ((m + 255) / 256) * ((p + 255) / 256);
+  if (tiles_one < 2 * (int64_t)(sms / 2)) {
+    ctx->res_mod = t.m[0];
+    ctx->res_nbat = L.nmod;
+    for (int l = 0; l < L.nmod; ++l) ctx->res_mods[l] = t.m[l];
+    ctx->res_bat_rows = L.mp;
+    ctx->res_bat_krows = L.kp;
+    st = gemm_ld(ctx, (int64_t)L.nmod * L.mp, L.kp, p, MM_S8_S32, Ar, L.kp, Br, L.pp, R, L.pp, 0, s);
     if (st != MM_OK) return st;
+  } else {
+    ctx->res_nbat = 1;
+    for (int l = 0; l < L.nmod; ++l) {
+      ctx->res_mod = t.m[l];
+      st = gemm_ld(ctx, m, L.kp, p, MM_S8_S32, Ar + (int64_t)l * L.mp * L.kp, L.kp, Br + (int64_t)l * L.kp * L.pp,
+                   L.pp, R + (int64_t)l * L.mp * L.pp, L.pp, 0, s);
+      if (st != MM_OK) return st;
+    }
   }
   ctx->res_mod = 0;
+  ctx->res_nbat = 0;
   // Chinese remaindering, scaling and the binary64 store
   switch (L.nmod) {
-    case 14: launch_combine<14>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
-    case 15: launch_combine<15>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
-    default: launch_combine<16>(R, m, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+    case 14: launch_combine<14>(R, m, L.mp, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+    case 15: launch_combine<15>(R, m, L.mp, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
+    default: launch_combine<16>(R, m, L.mp, p, L.pp, C, ldc, e, f, beta_one, t, sms, s); break;
   }
   return chk("CRT combine", 1);
 }

@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (diagnostics, MM_DEBUG bit 1: every tile reads the first tile's operands -> L2 hits only)
         const int m0 = ((args.debug & 2) ? 0 : tm * Cfg::M_TILE) + (int)pair * Cfg::M_MMA + (int)rank * Cfg::BM;
         const int n0 = ((args.debug & 2) ? 0 : tn * Cfg::TILE_N) + (int)rank * Cfg::BN_CTA;  // + rr * kBN for region rr
+        // batched residue products (MM_F64_EMU): this tile's batch reads its own B rows
+        const int kbat = args.bat_rows ? (tm * Cfg::M_TILE / args.bat_rows) * args.bat_krows : 0;
         for (int kb = kb0; kb < kb1; ++kb) {
           const uint64_t te0 = args.trace ? globaltimer_ns() : 0;
           if (!mbar_wait(empty_bar(stage), phase ^ 1u, err, 1)) { ok = false; break; }
@@ -263,14 +265,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_hint(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
-                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
+                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0 + kbat, pol_b);
             } else {
 #pragma unroll
               for (int a = 0; a < KA; ++a) tma_load_2d(sa + a * Cfg::A_ATOM, &tmA, full_bar(stage), k0 + a * Cfg::BKA, m0);
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d(sb + rb * Cfg::BOX_BYTES, &tmB, full_bar(stage),
-                            n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0);
+                            n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0 + kbat);
             }
           } else if constexpr (MC == 2) {
             // A: this CTA's own 128 rows.  B: this pair's half of the K rows of each box, multicast
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
               tma_load_2d_pair_mc(sb + rb * Cfg::BOX_BYTES + pair * Cfg::B_PART, &tmB, leader_full,
                                   n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN,
-                                  k0 + (int)pair * Cfg::BKB, mask);
+                                  k0 + kbat + (int)pair * Cfg::BKB, mask);
           } else if (NT == 1 && hf >= 0) {
             // N-half tail item: this CTA's 128 rows of A, and its 64 of the half's 128 columns of B
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int a = 0; a < KA; ++a)
               tma_load_2d_pair(sa + a * Cfg::A_ATOM, &tmA, leader_full, k0 + a * Cfg::BKA, m0);
-            tma_load_2d_pair(sb, &tmBh, leader_full, tn * Cfg::TILE_N + hf * (kBN / 2) + (int)rank * (kBN / 4), k0);
+            tma_load_2d_pair(sb, &tmBh, leader_full, tn * Cfg::TILE_N + hf * (kBN / 2) + (int)rank * (kBN / 4), k0 + kbat);
           } else {
             const uint32_t leader_full = mapa_shared(full_bar(stage), 0);
             if (rank == 0) mbar_arrive_expect_tx(full_bar(stage), 2 * Cfg::STAGE_BYTES);
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_pair_hint(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
-                                      n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0, pol_b);
+                                      n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0 + kbat, pol_b);
             } else {
 #pragma unroll
               for (int a = 0; a < KA; ++a)
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int rb = 0; rb < NT * Cfg::NBOX; ++rb)
                 tma_load_2d_pair(sb + rb * Cfg::BOX_BYTES, &tmB, leader_full,
-                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0);
+                                 n0 + (rb / Cfg::NBOX) * kBN + (rb % Cfg::NBOX) * Cfg::BOXN, k0 + kbat);
             }
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
@@ -452,6 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n_stores = 0;
     auto emit = [&](const uint32_t (&v)[32], int64_t row_base, int64_t col0, bool red = false) {
       if (I8 && args.res_m) {  // (compiled into the INT8 kernels only)
+        const int bb = args.bat_rows ? (int)(row_base / args.bat_rows) : 0;
+        const int rm = args.res_mt[bb], rc16 = args.res_c16t[bb];
+        const float rrcp = args.res_rcpt[bb];
         // MM_F64_EMU: the exact INT32 values reduced mod res_m to bytes — x = 2^16 h + l, y = h·(2^16
         // mod m) + l ≡ x (|y| < 2^24, exact in float), r = y − m·floor(y/m) corrected — 32 bytes per
         // row, staged unswizzled (32 rows × 32 B) and stored by one TMA store (uint8 map, no reduce-add)
@@ -462,10 +467,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int x = (int)v[4 * i + u];
-            const int y = (x >> 16) * args.res_c16 + (x & 0xFFFF);
-            int r = y - __float2int_rd(__int2float_rn(y) * args.res_rcp) * args.res_m;
-            r += r < 0 ? args.res_m : 0;
-            r -= r >= args.res_m ? args.res_m : 0;
+            const int y = (x >> 16) * rc16 + (x & 0xFFFF);
+            int r = y - __float2int_rd(__int2float_rn(y) * rrcp) * rm;
+            r += r < 0 ? rm : 0;
+            r -= r >= rm ? rm : 0;
             word |= (uint32_t)r << (8 * u);
           }
           w[i] = word;

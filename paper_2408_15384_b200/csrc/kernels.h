@@ -34,11 +34,15 @@ struct GemmArgs {
   int ka;           // tcgen05 kernel: 128-B K atoms per stage (1, or 2 for 256-wide pair tiles)
   int exp;          // schedule experiments that keep results exact (knob MM_EXP, A/B only; 0 = off)
   unsigned long long* clk;  // clock meter (mm_clock_meter): per CTA {clock64, globaltimer} at entry and exit, or null
-  // tcgen05 INT8 kernel, MM_F64_EMU's products: store C mod res_m (bytes in [0, res_m), C a uint8
-  // matrix) instead of the INT32 values; 0 = INT32 C
+  // tcgen05 INT8 kernel, MM_F64_EMU's products: store C mod m (bytes in [0, m), C a uint8 matrix)
+  // instead of the INT32 values (res_m = 0: INT32 C).  Batched (bat_rows > 0): C and A are stacks
+  // of batches of bat_rows rows (a multiple of the tile height), batch b's B starts at row
+  // b·bat_krows of the B map, and its modulus is res_mt[b]; else one batch with res_mt[0].
   int res_m;
-  int res_c16;    // 2^16 mod res_m
-  float res_rcp;  // 1 / res_m
+  int bat_rows, bat_krows;
+  int res_mt[16];
+  int res_c16t[16];    // 2^16 mod m
+  float res_rcpt[16];  // 1 / m
 };
 
 // FP64 launch plan (tile shape, stream-K grid, workspace needs).

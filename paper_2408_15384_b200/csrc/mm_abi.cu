@@ -294,8 +294,8 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
   a.ka = 1;
   a.clk = ctx->clk_on ? ctx->clk_buf : nullptr;
   a.res_m = 0;
-  a.res_c16 = 0;
-  a.res_rcp = 0.0f;
+  a.bat_rows = 0;
+  a.bat_krows = 0;
 #ifdef MM_DIAG
   if (const char* env = knob("MM_DEBUG")) a.debug = atoi(env);  // diagnostics: results are garbage
   const bool trace = knob("MM_TRACE") != nullptr && dtype != MM_F64;  // debug: per-role wait times
@@ -390,6 +390,7 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     const bool i8 = dtype == MM_S8_S32;
     int cg = force_cg();
     if (!cg) cg = (m <= 128) ? 1 : 2;
+    if (ctx->res_mod && ctx->res_nbat > 1) cg = 2;  // batched residue products: 256-row pair tiles
     // 512-wide tiles (two N=256 accumulators per CTA pair) for large operands: 25 % fewer
     // L2->SM bytes and DRAM re-reads per FLOP, at the price of no TMEM double-buffering.
     // ... and whenever they fill at least one wave of the pairs (measured 4096^3: int8 +3 %,
@@ -401,6 +402,7 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     // two CTA pairs per cluster sharing (multicasting) every B slab
     int mc = 1;
     if (const char* env = knob("MM_MC")) mc = (cg == 2 && m > 256 && atoi(env) == 2) ? 2 : 1;  // tuning knob
+    if (ctx->res_mod && ctx->res_nbat > 1) mc = 1;  // batched residue products: one pair per tile
     // With few waves of 512-wide tiles (quantisation, an exposed read-out per tile) 256-wide tiles
     // with TMEM double-buffering and two K atoms per stage win: int8 4096^3 +3 %, bf16 4096^3 +2 %;
     // from ~7 waves on (8192^3) 512-wide tiles stay ahead (tools/ab_gpu.py).
@@ -431,7 +433,9 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     st = encode_2d(ctx, &tmA, dt, esz, Ause, m, n, padA ? ldA2 : lda, abox, "A");
     if (st != MM_OK) return st;
-    st = encode_2d(ctx, &tmB, dt, esz, Buse, n, p, padB ? ldB2 : ldb, bbox, "B");
+    // batched residue products (MM_F64_EMU): B is a stack of res_nbat batches of res_bat_krows rows
+    const int64_t brows = ctx->res_mod && ctx->res_nbat > 1 ? (int64_t)ctx->res_nbat * ctx->res_bat_krows : n;
+    st = encode_2d(ctx, &tmB, dt, esz, Buse, brows, p, padB ? ldB2 : ldb, bbox, "B");
     if (st != MM_OK) return st;
     // C through TMA stores when its base and pitch allow (else predicated register stores)
     CUtensorMap tmC;
@@ -439,9 +443,20 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     if (ctx->res_mod) {  // MM_F64_EMU's products: C mod res_mod as bytes (uint8 C, TMA stores only)
       if (!i8 || !tma_ok(C, ldc, 1))
         return set_err(ctx, MM_ERR_RUNTIME, "internal: residue output needs an INT8 product and a TMA-storable C");
-      a.res_m = ctx->res_mod;
-      a.res_c16 = (int)(65536u % (unsigned)ctx->res_mod);
-      a.res_rcp = 1.0f / (float)ctx->res_mod;
+      a.res_m = 1;
+      const int nb = ctx->res_nbat > 1 ? ctx->res_nbat : 1;
+      for (int b = 0; b < 16; ++b) {
+        const int md = b < nb ? (nb > 1 ? ctx->res_mods[b] : ctx->res_mod) : 1;
+        a.res_mt[b] = md;
+        a.res_c16t[b] = (int)(65536u % (unsigned)md);
+        a.res_rcpt[b] = 1.0f / (float)md;
+      }
+      if (nb > 1) {  // batches stacked along M: whole 256-row pair tiles per batch, no multicast clusters
+        if (ctx->res_bat_rows % 256 != 0 || cg != 2 || mc != 1 || padB)
+          return set_err(ctx, MM_ERR_RUNTIME, "internal: batched residue products need 256-row batches and CTA pairs");
+        a.bat_rows = (int)ctx->res_bat_rows;
+        a.bat_krows = (int)ctx->res_bat_krows;
+      }
       a.no_reduce = 1;  // partial sums are added before the reduction, never in C
       a.c_tma = 1;
       const uint32_t rbox[2] = {32, 32};
@@ -462,7 +477,7 @@ mm_status gemm_ld_impl(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, mm_dtype dt
     CUtensorMap tmBh = tmB;
     if (i8 && cg == 2 && nt == 1 && mc == 1) {
       const uint32_t hbox[2] = {64, bbox[1]};
-      st = encode_2d(ctx, &tmBh, dt, esz, Buse, n, p, padB ? ldB2 : ldb, hbox, "B (64-column boxes)", 64);
+      st = encode_2d(ctx, &tmBh, dt, esz, Buse, brows, p, padB ? ldB2 : ldb, hbox, "B (64-column boxes)", 64);
       if (st != MM_OK) return st;
     }
     e = launch_gemm_tc(i8, cg, nt, mc, tmA, tmB, tmC, tmBh, a, num_sms, s);
@@ -684,10 +699,11 @@ int64_t product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
   }
   return pad + round_up(slabs, 256) + round_up(std::max<int64_t>(flags, 256), 256);
 }
-// MM_F64_EMU: residue planes + INT32 product + the INT8 product's own scratch
+// MM_F64_EMU: residue planes + the batched INT8 product's own scratch (N planes of whole 256-row tiles)
 int64_t emu_or_product_scratch(int64_t m, int64_t n, int64_t p, mm_dtype dt) {
   if (dt != MM_F64_EMU) return product_scratch(m, n, p, dt);
-  return (int64_t)f64_emu_scratch(m, n, p) + product_scratch(m, n, p, MM_S8_S32);
+  const int64_t nmod = f64_emu_moduli(n, nullptr, nullptr);
+  return (int64_t)f64_emu_scratch(m, n, p) + product_scratch(nmod * ((m + 255) / 256 * 256), (n + 15) / 16 * 16, p, MM_S8_S32);
 }
 }  // namespace
 
