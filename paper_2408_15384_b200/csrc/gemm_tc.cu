@@ -24,7 +24,10 @@
 //     a split last wave (sched.cuh modes) either adds partial slabs in a fixed
 //     order or, by default, adds exact K halves into C with TMA reduce-add;
 //   * edges (ragged m, n, p): TMA zero-fills out-of-bounds boxes (zeros add
-//     exactly 0 to every sum) and clips out-of-bounds stores.
+//     exactly 0 to every sum) and clips out-of-bounds stores;
+//   * INT8 only, for MM_F64_EMU (f64_emu.cu): the epilogue can store C mod m as bytes, and one
+//     launch can run a batch of products stacked along M, each with its own B rows and modulus
+//     (GemmArgs::res_m / bat_rows).
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator +
 // MMA issuer, warps 2..9 = epilogue (two per TMEM lane quarter).

@@ -797,13 +797,16 @@ def test_n_half_tail_same_bits_as_whole_tiles(mm, dt):
     check(dt, outs["4"][:64].cpu().numpy(), Cref, D, exact=False)
 
 
-@pytest.mark.parametrize("shape", [(256, 256, 256), (2000, 1500, 1750), (1000, 333, 517), (37, 4100, 29), (1, 1, 1)])
+@pytest.mark.parametrize("shape", [(256, 256, 256), (2000, 1500, 1750), (1000, 333, 517), (37, 4100, 29), (1, 1, 1),
+                                   (3300, 700, 3100)])
 def test_f64_emulation(mm, shape):
     """MM_F64_EMU (f64_emu.cu): the binary64 product on the INT8 tensor cores (integer scaling,
     residues modulo 14-16 coprime moduli, one exact INT8 product per modulus, Chinese remaindering).
     Exact-integer inputs (|x| <= 1024, K = 2049 pins) bit-exact — the scaling leaves integers
     unrounded and the remaindering is exact; U[-1,1) inputs within the FP64 tolerance of the oracle
-    and, diagnostically, of DMMA's ~1e-16; ragged n (K padding) and p % 16 != 0 (padded planes)."""
+    and, diagnostically, of DMMA's ~1e-16; ragged n (K padding) and p % 16 != 0 (padded planes).
+    Below two waves of tiles the N products run as one batched launch; 3300x700x3100 (169 tiles)
+    takes the N-launch path."""
     m, n, p = shape
     A, B = gen("f64", "exact", 71, m, n, p, 2049)
     Cref, _ = ref("f64", A, B)
