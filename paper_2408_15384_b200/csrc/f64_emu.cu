@@ -31,6 +31,7 @@
 
 #include "ctx.h"
 #include "kernels.h"
+#include "knobs.h"
 
 namespace mmb {
 
@@ -444,7 +445,9 @@ mm_status gemm_f64_emu(mm_ctx* ctx, int64_t m, int64_t n, int64_t p, const doubl
     ~ResetRes() { c->res_mod = 0; c->res_nbat = 0; }
   } reset{ctx};
   const int64_t tiles_one = ((m + 255) / 256) * ((p + 255) / 256);
-  if (tiles_one < 2 * (int64_t)(sms / 2)) {
+  bool batched = tiles_one < 2 * (int64_t)(sms / 2);
+  if (const char* e = knob("MM_EMU_BATCH")) batched = atoi(e) != 0;  // tuning knob (A/B)
+  if (batched) {
     ctx->res_mod = t.m[0];
     ctx->res_nbat = L.nmod;
     for (int l = 0; l < L.nmod; ++l) ctx->res_mods[l] = t.m[l];
