@@ -63,11 +63,14 @@ struct F64Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // ~200 KB of operand ring: 6 stages at 128x128, 12 at 64x64, 25 at 32x32 (a whole K <= 384 of a
   // small tile in flight at once: the cold DRAM round trip is paid once, not K/(16*stages) times)
-  static constexpr int STAGES0 = (200 * 1024) / STAGE_BYTES < 64 ? (200 * 1024) / STAGE_BYTES : 64;
-  static constexpr int STAGES = STAGES0 / KB * KB;            // whole groups of KB slots
-  static constexpr int BOX_STRIDE = KB * BBOX_BYTES;          // between B column boxes of one slot
   static constexpr int SCR_BYTES = (KS - 1) * BM * BN * 8;  // accumulators of groups 1..KS-1
   static constexpr int XSCR_BYTES = (CK - 1) * BM * BN * 8;  // rank 0: the other K half's partial tile
+  // (and never more than the 227 KB a CTA may hold with the scratch: KS = 8 has 56 KB of it)
+  static constexpr int RING_MAX = 225 * 1024 - 2048 - SCR_BYTES - XSCR_BYTES;
+  static constexpr int RING = (200 * 1024) < RING_MAX ? (200 * 1024) : RING_MAX;
+  static constexpr int STAGES0 = RING / STAGE_BYTES < 64 ? RING / STAGE_BYTES : 64;
+  static constexpr int STAGES = STAGES0 / KB * KB;            // whole groups of KB slots
+  static constexpr int BOX_STRIDE = KB * BBOX_BYTES;          // between B column boxes of one slot
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + SCR_BYTES + XSCR_BYTES + 1024;
   static_assert(STAGES >= 4 && 16 * STAGES <= 1008, "ring (+ the ticket word at the end of the barrier area)");
   static constexpr int MI = BM / WM / 8;  // 8-row DMMA tiles per warp
