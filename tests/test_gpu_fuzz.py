@@ -32,6 +32,8 @@ KNOBS_F64 = {
     "MM_F64_STREAMK": [None, "0", "1"],
     "MM_F64_W8": [None, None, None, "1"],
     "MM_F64_CK": [None, None, "1"],
+    "MM_F64_KS": [None, None, None, "2", "4", "8", "44"],
+    "MM_F64_KB": [None, None, "1"],
 }
 
 
